@@ -1,0 +1,1206 @@
+// capi.cu -- the C ABI (include/vegas_b200.h): contexts, the per-iteration
+// launch sequence, NCCL merge, and the stateless parity entry points.
+//
+// One iteration (vp/core.py:200-219) on the context's stream, no host sync:
+//   map     plan_scan_kernel + plan_offsets_kernel      (strat.build_run_plan)
+//   fill    fill_kernel + fill_fixup + hist_reduce      (executor.parallel_fill)
+//           [+ ncclAllReduce of map_w|s1|s2 and map_counts]  (tree_reduce)
+//   update  results_leaf + results_tree                 (strat.compute_results)
+//           alloc_kernel                                (update_evals_per_cube)
+//           refine_kernel                               (smooth_and_damp + update_grid)
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/vegas_b200.h"
+#include "fill_launch.h"
+#include "update.cuh"
+
+using namespace vpb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(VPB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define NK(x)                                                                          \
+  do {                                                                                 \
+    ncclResult_t r_ = (x);                                                             \
+    if (r_ != ncclSuccess)                                                             \
+      return fail(VPB_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+#define TRY(x)                   \
+  do {                           \
+    int rc_ = (x);               \
+    if (rc_ != VPB_OK) return rc_; \
+  } while (0)
+
+// ------------------------------------------------------------ pairwise plan --
+// numpy's recursive split (n > 128 -> n2 = n/2 - (n/2)%8) flattened into
+// leaves (in order) and inner nodes grouped by height.
+struct PwPlan {
+  std::vector<long long> leaf_off;
+  std::vector<int> leaf_len;
+  std::vector<int> node_l, node_r, level_start;
+  int L = 0, I = 0, H = 0;
+  // device copies
+  long long *d_leaf_off = nullptr;
+  int *d_leaf_len = nullptr, *d_node_l = nullptr, *d_node_r = nullptr, *d_level = nullptr;
+
+  void build(long long n) {
+    struct Node { int l, r, h; };
+    std::vector<Node> inner;
+    std::vector<long long> lo;
+    std::vector<int> ll;
+    // returns (id, height); ids: leaves >= 0 in leaf order, inner encoded as -(k+1)
+    std::function<std::pair<int, int>(long long, long long)> rec =
+        [&](long long off, long long m) -> std::pair<int, int> {
+      if (m <= 128) {
+        lo.push_back(off);
+        ll.push_back((int)m);
+        return {(int)lo.size() - 1, 0};
+      }
+      long long n2 = m / 2;
+      n2 -= n2 % 8;
+      auto a = rec(off, n2);
+      auto b = rec(off + n2, m - n2);
+      inner.push_back({a.first, b.first, std::max(a.second, b.second) + 1});
+      return {-(int)inner.size(), inner.back().h};
+    };
+    rec(0, n);
+    L = (int)lo.size();
+    I = (int)inner.size();
+    // order inner nodes by height (stable), remap ids
+    std::vector<int> order(I);
+    for (int i = 0; i < I; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return inner[a].h < inner[b].h; });
+    std::vector<int> pos(I);
+    for (int i = 0; i < I; i++) pos[order[i]] = i;
+    auto map_id = [&](int id) { return id >= 0 ? id : L + pos[-id - 1]; };
+    node_l.resize(I);
+    node_r.resize(I);
+    H = I ? inner[order[I - 1]].h : 0;
+    level_start.assign(H + 1, 0);
+    for (int i = 0; i < I; i++) {
+      const Node &nd = inner[order[i]];
+      node_l[i] = map_id(nd.l);
+      node_r[i] = map_id(nd.r);
+    }
+    // level_start[h-1] = first inner node with height h
+    for (int h = 1; h <= H; h++) {
+      int k = 0;
+      while (k < I && inner[order[k]].h < h) k++;
+      level_start[h - 1] = k;
+    }
+    level_start[H] = I;
+    // the root must be the last inner node (the unique node of max height)
+    leaf_off = lo;
+    leaf_len = ll;
+  }
+  int upload() {
+    CK(cudaMalloc(&d_leaf_off, sizeof(long long) * std::max(L, 1)));
+    CK(cudaMalloc(&d_leaf_len, sizeof(int) * std::max(L, 1)));
+    CK(cudaMalloc(&d_node_l, sizeof(int) * std::max(I, 1)));
+    CK(cudaMalloc(&d_node_r, sizeof(int) * std::max(I, 1)));
+    CK(cudaMalloc(&d_level, sizeof(int) * (H + 1)));
+    CK(cudaMemcpy(d_leaf_off, leaf_off.data(), sizeof(long long) * L, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_leaf_len, leaf_len.data(), sizeof(int) * L, cudaMemcpyHostToDevice));
+    if (I) {
+      CK(cudaMemcpy(d_node_l, node_l.data(), sizeof(int) * I, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_node_r, node_r.data(), sizeof(int) * I, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(d_level, level_start.data(), sizeof(int) * (H + 1), cudaMemcpyHostToDevice));
+    return VPB_OK;
+  }
+  PwPlanDev dev() const {
+    return {d_leaf_off, d_leaf_len, d_node_l, d_node_r, d_level, L, I, H};
+  }
+  void release() {
+    cudaFree(d_leaf_off); cudaFree(d_leaf_len); cudaFree(d_node_l); cudaFree(d_node_r);
+    cudaFree(d_level);
+    d_leaf_off = nullptr;
+  }
+};
+
+template <class T>
+int dalloc(T **p, size_t n) {
+  CK(cudaMalloc((void **)p, sizeof(T) * std::max<size_t>(n, 1)));
+  return VPB_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- context --
+struct vpb_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int dims = 0, ng = 0, id = 0, max_it = 0;
+  long long ns = 1, n_cubes = 1, n_eval = 0, batch = 1;
+  unsigned long long seed = 0;
+  double alpha = 0.5, beta = 0.75;
+  IParams P{};
+  std::vector<double> bounds;
+  long long uniform_nh = 2;
+  long long nb = 1;            // plan blocks
+  long long ntiles_cap = 1;
+  // device state
+  double *edges = nullptr;
+  long long *n_h = nullptr, *offsets = nullptr, *bsum = nullptr;
+  double *accf = nullptr;       // [map_w | s1 | s2]
+  double *map_w = nullptr, *s1 = nullptr, *s2 = nullptr;
+  long long *map_counts = nullptr;
+  double *d_h = nullptr, *dp = nullptr, *pwvals = nullptr;
+  PwPlan pw;
+  Sched *sched = nullptr;
+  Scalars *sc = nullptr;
+  double *h_est = nullptr, *h_var = nullptr;
+  long long *h_evals = nullptr;
+  int *tile_cube = nullptr;
+  long long *ck_head = nullptr, *ck_tail = nullptr;
+  double *cv_head = nullptr, *cv_tail = nullptr;
+  int *ct_through = nullptr;
+  double *hw_part = nullptr, *hw_glob = nullptr;
+  unsigned *hc_part = nullptr;
+  unsigned long long *hc_glob = nullptr;
+  int *status = nullptr, *fail_it = nullptr;
+  unsigned long long *err_run = nullptr;
+  double *refine_scr = nullptr;
+  long long *explicit_rb = nullptr;
+  // fill launch geometry
+  int grid = 0;
+  bool smem_hist = true;
+  size_t smem = 0;
+  // multi-GPU
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  // timing
+  std::vector<std::array<cudaEvent_t, 4>> ev;
+  cudaEvent_t f0 = nullptr, f1 = nullptr;
+  int it_enq = 0;   // iterations enqueued since reset
+};
+
+namespace {
+
+FillArgs fill_args(vpb_ctx *c) {
+  FillArgs a{};
+  a.offsets = c->offsets;
+  a.n_cubes = c->n_cubes;
+  a.edges = c->edges;
+  a.dims = c->dims;
+  a.ng = c->ng;
+  a.n_strat = c->ns;
+  a.nsf = (double)c->ns;
+  a.rns = 1.0 / (double)c->ns;
+  a.ngf = (double)c->ng;
+  a.batch = c->batch;
+  a.seed = c->seed;
+  const unsigned long long step = (unsigned long long)c->grid * FILL_TILE;
+  a.dk = (long long)(step / (unsigned long long)c->batch);
+  a.ds = (long long)(step % (unsigned long long)c->batch);
+  a.sched = c->sched;
+  a.tile_cube = c->tile_cube;
+  a.s1 = c->s1;
+  a.s2 = c->s2;
+  a.ck_head = c->ck_head;
+  a.ck_tail = c->ck_tail;
+  a.cv_head = c->cv_head;
+  a.cv_tail = c->cv_tail;
+  a.ct_through = c->ct_through;
+  a.hw_part = c->hw_part;
+  a.hc_part = c->hc_part;
+  a.hw_glob = c->hw_glob;
+  a.hc_glob = c->hc_glob;
+  a.smem_hist = c->smem_hist ? 1 : 0;
+  a.status = c->status;
+  a.err_run = c->err_run;
+  a.P = c->P;
+  return a;
+}
+
+int setdev(vpb_ctx *c) {
+  CK(cudaSetDevice(c->dev));
+  return VPB_OK;
+}
+
+// plan kernels: block sums must already be in c->bsum (alloc_kernel or
+// nh_blocksum_kernel); explicit run_base (device pointer) or nullptr.
+int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
+  plan_scan_kernel<<<1, PLAN_NT, 0, c->st>>>(c->bsum, c->nb, c->sched, c->world, c->rank,
+                                             c->h_evals, record, c->ntiles_cap, c->status,
+                                             explicit_rb);
+  plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,
+                                                             c->offsets, c->sched, c->tile_cube);
+  CK(cudaGetLastError());
+  return VPB_OK;
+}
+
+int enqueue_fill(vpb_ctx *c, bool timed) {
+  const size_t m = (size_t)c->dims * c->ng;
+  CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
+  if (!c->smem_hist) {
+    CK(cudaMemsetAsync(c->hw_glob, 0, sizeof(double) * m, c->st));
+    CK(cudaMemsetAsync(c->hc_glob, 0, sizeof(unsigned long long) * m, c->st));
+  }
+  FillArgs a = fill_args(c);
+  if (timed) CK(cudaEventRecord(c->f0, c->st));
+  CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+  if (timed) CK(cudaEventRecord(c->f1, c->st));
+  const long long nt = c->ntiles_cap;
+  fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
+  if (c->smem_hist) {
+    hist_reduce_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->st>>>(
+        c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
+  } else {
+    CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, c->st));
+    hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->st>>>(c->hc_glob,
+                                                                           (long long)m,
+                                                                           c->map_counts);
+  }
+  CK(cudaGetLastError());
+  if (c->comm) {
+    NK(ncclGroupStart());
+    NK(ncclAllReduce(c->accf, c->accf, m + 2 * (size_t)c->n_cubes, ncclFloat64, ncclSum, c->comm,
+                     c->st));
+    NK(ncclAllReduce(c->map_counts, c->map_counts, m, ncclInt64, ncclSum, c->comm, c->st));
+    NK(ncclGroupEnd());
+  }
+  return VPB_OK;
+}
+
+int enqueue_update(vpb_ctx *c, int record) {
+  const double V = 1.0 / (double)c->n_cubes;
+  const PwPlanDev pd = c->pw.dev();
+  results_leaf_kernel<<<(unsigned)((pd.L + 127) / 128), 128, 0, c->st>>>(
+      c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, pd, c->d_h, c->dp, c->pwvals, c->status);
+  results_tree_kernel<<<1, 1024, 0, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
+                                             c->h_var, c->sched, c->status, record);
+  alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, c->beta,
+                                                       (double)c->n_eval, c->uniform_nh, c->sc, 0,
+                                                       c->n_h, c->bsum, c->status);
+  refine_kernel<<<c->dims, 256, 0, c->st>>>(c->edges, c->map_w, c->map_counts, c->ng, c->alpha,
+                                            c->refine_scr, c->status, nullptr);
+  CK(cudaGetLastError());
+  return VPB_OK;
+}
+
+__global__ void mark_fail_kernel(const int *status, int *fail_it, const Sched *sched) {
+  if (*status && *fail_it < 0) *fail_it = sched->it;
+}
+__global__ void guarded_set_it_kernel(Sched *sched, int it, const int *status) {
+  if (!*status) sched->it = it;
+}
+
+int enqueue_iteration(vpb_ctx *c) {
+  if (c->it_enq >= c->max_it)
+    return fail(VPB_ERR_INVALID, "iteration history capacity (max_it) exhausted");
+  auto &E = c->ev[c->it_enq];
+  guarded_set_it_kernel<<<1, 1, 0, c->st>>>(c->sched, c->it_enq, c->status);
+  CK(cudaEventRecord(E[0], c->st));
+  TRY(enqueue_plan(c, 1, nullptr));
+  CK(cudaEventRecord(E[1], c->st));
+  TRY(enqueue_fill(c, true));
+  CK(cudaEventRecord(E[2], c->st));
+  TRY(enqueue_update(c, 1));
+  CK(cudaEventRecord(E[3], c->st));
+  mark_fail_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
+  CK(cudaGetLastError());
+  c->it_enq++;
+  return VPB_OK;
+}
+
+int uniform_allocation(vpb_ctx *c) {
+  alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, 0.0, (double)c->n_eval,
+                                                       c->uniform_nh, c->sc, 1, c->n_h, c->bsum,
+                                                       c->status);
+  CK(cudaGetLastError());
+  return VPB_OK;
+}
+
+int upload_uniform_edges(vpb_ctx *c) {
+  // maps.new_uniform (vp/maps.py:70-88): np.linspace(lo, hi, ng+1) with exact
+  // endpoints.  numpy's linspace: step = (hi-lo)/ng; y = arange(0, ng+1)*step + lo;
+  // last element forced to hi.
+  std::vector<double> e((size_t)c->dims * (c->ng + 1));
+  for (int j = 0; j < c->dims; j++) {
+    const double lo = c->bounds[2 * j], hi = c->bounds[2 * j + 1];
+    const double delta = hi - lo;
+    const double step = delta / c->ng;
+    for (int i = 0; i <= c->ng; i++) {
+      double v;
+      if (step == 0.0) v = ((double)i / c->ng) * delta + lo;
+      else v = (double)i * step + lo;
+      e[(size_t)j * (c->ng + 1) + i] = v;
+    }
+    e[(size_t)j * (c->ng + 1)] = lo;
+    e[(size_t)j * (c->ng + 1) + c->ng] = hi;
+  }
+  CK(cudaMemcpyAsync(c->edges, e.data(), sizeof(double) * e.size(), cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return VPB_OK;
+}
+
+void free_ctx(vpb_ctx *c) {
+  void *ptrs[] = {c->edges, c->n_h, c->offsets, c->bsum, c->accf, c->map_counts, c->d_h, c->dp,
+                  c->pwvals, c->sched, c->sc, c->h_est, c->h_var, c->h_evals, c->tile_cube,
+                  c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
+                  c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
+                  c->refine_scr, c->explicit_rb};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  c->pw.release();
+  for (auto &E : c->ev)
+    for (auto e : E)
+      if (e) cudaEventDestroy(e);
+  if (c->f0) cudaEventDestroy(c->f0);
+  if (c->f1) cudaEventDestroy(c->f1);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+}
+
+int validate_desc(const vpb_desc *d) {
+  if (!d) return fail(VPB_ERR_INVALID, "null descriptor");
+  if (d->dims < 1 || d->dims > VPB_MAX_DIMS)
+    return fail(VPB_ERR_INVALID, "dims must be in [1, 64]");
+  if (d->n_intervals < 2) return fail(VPB_ERR_INVALID, "n_intervals must be >= 2");
+  if (d->n_strat < 1) return fail(VPB_ERR_INVALID, "n_strat must be >= 1");
+  if (d->n_eval < 4) return fail(VPB_ERR_INVALID, "n_eval must be >= 4");
+  if (d->batch_size < 1) return fail(VPB_ERR_INVALID, "batch_size must be >= 1");
+  if (!(d->alpha >= 0) || !(d->beta >= 0)) return fail(VPB_ERR_INVALID, "alpha and beta must be >= 0");
+  if (d->integrand < 0 || d->integrand >= VPB_N_INTEGRANDS)
+    return fail(VPB_ERR_UNSUPPORTED, "unknown integrand id");
+  if (d->n_params < 0 || d->n_params > VPB_MAX_PARAMS)
+    return fail(VPB_ERR_INVALID, "too many integrand parameters");
+  if (!d->bounds) return fail(VPB_ERR_INVALID, "bounds required");
+  if (d->max_it < 1) return fail(VPB_ERR_INVALID, "max_it must be >= 1");
+  // n_cubes = n_strat^dims must fit comfortably
+  double nc = std::pow((double)d->n_strat, (double)d->dims);
+  if (nc > 2147483647.0) return fail(VPB_ERR_INVALID, "n_strat**dims exceeds 2^31 cubes");
+  return VPB_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ exports --
+// (C linkage comes from the extern "C" declarations in vegas_b200.h)
+
+int vpb_abi_version(void) { return VPB_ABI_VERSION; }
+const char *vpb_last_error(void) { return g_err.c_str(); }
+int vpb_is_specialised(int32_t integrand, int32_t dims) {
+  return fill_is_specialised(integrand, dims);
+}
+
+int vpb_create(const vpb_desc *d, vpb_ctx **out) {
+  TRY(validate_desc(d));
+  if (!out) return fail(VPB_ERR_INVALID, "null output pointer");
+  auto *c = new vpb_ctx();
+  auto bail = [&](int rc) {
+    free_ctx(c);
+    delete c;
+    return rc;
+  };
+  if (d->device >= 0) c->dev = d->device;
+  else if (cudaGetDevice(&c->dev) != cudaSuccess) return bail(fail(VPB_ERR_CUDA, "no CUDA device"));
+  if (cudaSetDevice(c->dev) != cudaSuccess) return bail(fail(VPB_ERR_CUDA, "cudaSetDevice failed"));
+  c->dims = d->dims;
+  c->ng = d->n_intervals;
+  c->ns = d->n_strat;
+  c->n_eval = d->n_eval;
+  c->batch = d->batch_size;
+  c->seed = d->seed;
+  c->alpha = d->alpha;
+  c->beta = d->beta;
+  c->id = d->integrand;
+  c->max_it = d->max_it;
+  c->P.n = d->n_params;
+  for (int i = 0; i < d->n_params; i++) c->P.p[i] = d->params[i];
+  c->bounds.assign(d->bounds, d->bounds + 2 * d->dims);
+  for (int j = 0; j < d->dims; j++) {
+    const double lo = c->bounds[2 * j], hi = c->bounds[2 * j + 1];
+    if (!std::isfinite(lo) || !std::isfinite(hi) || !(lo < hi))
+      return bail(fail(VPB_ERR_INVALID, "bad bounds for dimension " + std::to_string(j)));
+  }
+  long long nc = 1;
+  for (int j = 0; j < d->dims; j++) nc *= d->n_strat;
+  c->n_cubes = nc;
+  {  // uniform share, vp/strat.py:101-102 + 111-112
+    const double p = 1.0 / (double)nc;
+    long long v = (long long)std::ceil((double)d->n_eval * p);
+    c->uniform_nh = v < 2 ? 2 : v;
+  }
+  c->nb = (nc + PLAN_NT - 1) / PLAN_NT;
+  // Σ n_h <= n_eval + 2 n_cubes (vp/strat.py:96-97); user allocations are checked
+  c->ntiles_cap = (d->n_eval + 2 * nc) / FILL_TILE + 2;
+  if (d->stream) {
+    c->st = (cudaStream_t)d->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(VPB_ERR_CUDA, "stream creation failed"));
+    c->own_stream = true;
+  }
+  const size_t m = (size_t)c->dims * c->ng;
+  int rc = VPB_OK;
+#define A(p, n) if ((rc = dalloc(&(p), (n))) != VPB_OK) return bail(rc)
+  A(c->edges, (size_t)c->dims * (c->ng + 1));
+  A(c->n_h, nc);
+  A(c->offsets, nc + 1);
+  A(c->bsum, c->nb);
+  A(c->accf, m + 2 * nc);
+  c->map_w = c->accf;
+  c->s1 = c->accf + m;
+  c->s2 = c->s1 + nc;
+  A(c->map_counts, m);
+  A(c->d_h, nc);
+  A(c->dp, nc);
+  c->pw.build(nc);
+  if ((rc = c->pw.upload()) != VPB_OK) return bail(rc);
+  A(c->pwvals, 3 * (size_t)(c->pw.L + c->pw.I));
+  A(c->sched, 1);
+  A(c->sc, 1);
+  A(c->h_est, c->max_it);
+  A(c->h_var, c->max_it);
+  A(c->h_evals, c->max_it);
+  A(c->tile_cube, c->ntiles_cap + 1);
+  A(c->ck_head, c->ntiles_cap);
+  A(c->ck_tail, c->ntiles_cap);
+  A(c->cv_head, 2 * c->ntiles_cap);
+  A(c->cv_tail, 2 * c->ntiles_cap);
+  A(c->ct_through, c->ntiles_cap);
+  A(c->status, 1);
+  A(c->fail_it, 1);
+  A(c->err_run, 1);
+  A(c->refine_scr, (size_t)c->dims * (5 * c->ng + 2));
+  A(c->explicit_rb, 1);
+  // fill geometry: shared histograms when they fit next to the edges
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+  c->smem_hist = true;
+  c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1);
+  if (c->smem > (size_t)optin) {
+    c->smem_hist = false;
+    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0);
+  }
+  if (c->smem > (size_t)optin)
+    return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
+  int per_sm = 0;
+  if (fill_occupancy(c->id, c->dims, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
+    return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
+  c->grid = sms * per_sm;
+  if (c->smem_hist) {
+    A(c->hw_part, (size_t)c->grid * m);
+    A(c->hc_part, (size_t)c->grid * m);
+  } else {
+    A(c->hw_glob, m);
+    A(c->hc_glob, m);
+  }
+#undef A
+  c->ev.resize(c->max_it);
+  for (auto &E : c->ev)
+    for (auto &e : E)
+      if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(VPB_ERR_CUDA, "event creation"));
+  if (cudaEventCreate(&c->f0) != cudaSuccess || cudaEventCreate(&c->f1) != cudaSuccess)
+    return bail(fail(VPB_ERR_CUDA, "event creation"));
+  if ((rc = vpb_reset(c)) != VPB_OK) return bail(rc);
+  *out = c;
+  return VPB_OK;
+}
+
+int vpb_destroy(vpb_ctx *c) {
+  if (!c) return VPB_OK;
+  cudaSetDevice(c->dev);
+  if (c->st) cudaStreamSynchronize(c->st);
+  free_ctx(c);
+  delete c;
+  return VPB_OK;
+}
+
+int vpb_nccl_unique_id(char id_out[128]) {
+  ncclUniqueId id;
+  NK(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  std::memcpy(id_out, &id, 128);
+  return VPB_OK;
+}
+
+int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
+  TRY(setdev(c));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->comm = nullptr;
+  NK(ncclCommInitRank(&c->comm, world, uid, rank));
+  c->world = world;
+  c->rank = rank;
+  return VPB_OK;
+}
+
+int vpb_set_shard(vpb_ctx *c, int32_t world, int32_t rank) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
+  c->world = world;
+  c->rank = rank;
+  return VPB_OK;
+}
+
+int vpb_reset(vpb_ctx *c) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  TRY(upload_uniform_edges(c));
+  Sched s{};
+  CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
+  Scalars z{};
+  CK(cudaMemcpy(c->sc, &z, sizeof(z), cudaMemcpyHostToDevice));
+  CK(cudaMemset(c->status, 0, sizeof(int)));
+  int m1 = -1;
+  CK(cudaMemcpy(c->fail_it, &m1, sizeof(int), cudaMemcpyHostToDevice));
+  unsigned long long big = ~0ull;
+  CK(cudaMemcpy(c->err_run, &big, sizeof(big), cudaMemcpyHostToDevice));
+  CK(cudaMemset(c->h_evals, 0, sizeof(long long) * c->max_it));
+  TRY(uniform_allocation(c));
+  CK(cudaStreamSynchronize(c->st));
+  c->it_enq = 0;
+  return VPB_OK;
+}
+
+int vpb_iterate(vpb_ctx *c, int32_t n_it) {
+  TRY(setdev(c));
+  for (int i = 0; i < n_it; i++) TRY(enqueue_iteration(c));
+  return VPB_OK;
+}
+
+int vpb_sync(vpb_ctx *c) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  return VPB_OK;
+}
+
+int vpb_history(vpb_ctx *c, int32_t cap, double *est, double *var, int64_t *evals,
+                int32_t *n_out) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  int status = 0, fit = -1;
+  CK(cudaMemcpy(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&fit, c->fail_it, sizeof(int), cudaMemcpyDeviceToHost));
+  int n = c->it_enq;
+  if (status && fit >= 0) n = fit;
+  n = std::min(n, (int)cap);
+  if (n > 0) {
+    if (est) CK(cudaMemcpy(est, c->h_est, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (var) CK(cudaMemcpy(var, c->h_var, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (evals) CK(cudaMemcpy(evals, c->h_evals, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+  }
+  if (n_out) *n_out = n;
+  if (status & 1)
+    return fail(VPB_ERR_NONFINITE, "integrand returned a non-finite value in iteration " +
+                                       std::to_string(fit + 1));
+  if (status & 2)
+    return fail(VPB_ERR_ASSERT, "grid update lost strict monotonicity (iteration " +
+                                    std::to_string(fit + 1) + ")");
+  return VPB_OK;
+}
+
+int vpb_error_info(vpb_ctx *c, int64_t *run_index, double *point, double *value) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  unsigned long long r = 0;
+  CK(cudaMemcpy(&r, c->err_run, sizeof(r), cudaMemcpyDeviceToHost));
+  if (r == ~0ull) return fail(VPB_ERR_INVALID, "no non-finite evaluation recorded");
+  Sched s;
+  CK(cudaMemcpy(&s, c->sched, sizeof(s), cudaMemcpyDeviceToHost));
+  double *x = nullptr, *jac = nullptr, *f = nullptr;
+  long long *idx = nullptr, *cube = nullptr;
+  int rc = VPB_OK;
+  if ((rc = dalloc(&x, c->dims)) || (rc = dalloc(&jac, 1)) || (rc = dalloc(&f, 1)) ||
+      (rc = dalloc(&idx, c->dims)) || (rc = dalloc(&cube, 1)))
+    return rc;
+  sample_runs_kernel<<<1, 1, 0, c->st>>>(c->seed, c->batch, s.run_base, (long long)r, 1,
+                                         c->offsets, c->n_cubes, c->edges, c->dims, c->ng, c->ns,
+                                         x, jac, idx, cube);
+  CK(cudaStreamSynchronize(c->st));
+  std::vector<double> hx(c->dims);
+  CK(cudaMemcpy(hx.data(), x, sizeof(double) * c->dims, cudaMemcpyDeviceToHost));
+  cudaFree(jac); cudaFree(idx); cudaFree(cube); cudaFree(f); cudaFree(x);
+  double v = 0.0;
+  std::vector<double> pp(c->P.p, c->P.p + c->P.n);
+  TRY(vpb_eval_host(c->id, pp.data(), c->P.n, hx.data(), 1, c->dims, &v));
+  if (run_index) *run_index = (int64_t)r;
+  if (point) std::memcpy(point, hx.data(), sizeof(double) * c->dims);
+  if (value) *value = v;
+  return VPB_OK;
+}
+
+int vpb_phase_times(vpb_ctx *c, double *map_ms, double *fill_ms, double *update_ms) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  double a = 0, b = 0, u = 0;
+  for (int i = 0; i < c->it_enq; i++) {
+    float t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][0], c->ev[i][1])); a += t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][1], c->ev[i][2])); b += t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][2], c->ev[i][3])); u += t;
+  }
+  if (map_ms) *map_ms = a;
+  if (fill_ms) *fill_ms = b;
+  if (update_ms) *update_ms = u;
+  return VPB_OK;
+}
+
+int vpb_last_fill_ms(vpb_ctx *c, double *ms) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  float t = 0;
+  CK(cudaEventElapsedTime(&t, c->f0, c->f1));
+  *ms = t;
+  return VPB_OK;
+}
+
+int vpb_set_edges(vpb_ctx *c, const double *edges) {
+  TRY(setdev(c));
+  CK(cudaMemcpyAsync(c->edges, edges, sizeof(double) * c->dims * (c->ng + 1),
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return VPB_OK;
+}
+
+int vpb_get_edges(vpb_ctx *c, double *edges) {
+  TRY(setdev(c));
+  CK(cudaMemcpyAsync(edges, c->edges, sizeof(double) * c->dims * (c->ng + 1),
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return VPB_OK;
+}
+
+int vpb_set_allocation(vpb_ctx *c, const int64_t *n_h) {
+  TRY(setdev(c));
+  long long tot = 0;
+  for (long long h = 0; h < c->n_cubes; h++) {
+    if (n_h[h] < 1) return fail(VPB_ERR_INVALID, "n_h entries must be >= 1");
+    tot += n_h[h];
+  }
+  if (tot / FILL_TILE + 2 > c->ntiles_cap)
+    return fail(VPB_ERR_INVALID, "allocation exceeds n_eval + 2*n_cubes");
+  CK(cudaMemcpyAsync(c->n_h, n_h, sizeof(long long) * c->n_cubes, cudaMemcpyHostToDevice, c->st));
+  nh_blocksum_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->st));
+  return VPB_OK;
+}
+
+int vpb_get_plan(vpb_ctx *c, int64_t *n_h, int64_t *offsets) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  if (n_h) CK(cudaMemcpy(n_h, c->n_h, sizeof(long long) * c->n_cubes, cudaMemcpyDeviceToHost));
+  if (offsets)
+    CK(cudaMemcpy(offsets, c->offsets, sizeof(long long) * (c->n_cubes + 1),
+                  cudaMemcpyDeviceToHost));
+  return VPB_OK;
+}
+
+int vpb_get_spread(vpb_ctx *c, double *d_h) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaMemcpy(d_h, c->d_h, sizeof(double) * c->n_cubes, cudaMemcpyDeviceToHost));
+  return VPB_OK;
+}
+
+int vpb_get_fill(vpb_ctx *c, double *map_w, int64_t *map_counts, double *s1, double *s2,
+                 int64_t *counts) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  const size_t m = (size_t)c->dims * c->ng;
+  if (map_w) CK(cudaMemcpy(map_w, c->map_w, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  if (map_counts)
+    CK(cudaMemcpy(map_counts, c->map_counts, sizeof(long long) * m, cudaMemcpyDeviceToHost));
+  if (s1) CK(cudaMemcpy(s1, c->s1, sizeof(double) * c->n_cubes, cudaMemcpyDeviceToHost));
+  if (s2) CK(cudaMemcpy(s2, c->s2, sizeof(double) * c->n_cubes, cudaMemcpyDeviceToHost));
+  if (counts) {
+    // every run of the plan is evaluated once: counts[h] = |[off_h, off_h+1) ∩ [lo, hi)|
+    // (summed over ranks after the all-reduce: n_h)
+    Sched s;
+    CK(cudaMemcpy(&s, c->sched, sizeof(s), cudaMemcpyDeviceToHost));
+    std::vector<long long> off(c->n_cubes + 1);
+    CK(cudaMemcpy(off.data(), c->offsets, sizeof(long long) * (c->n_cubes + 1),
+                  cudaMemcpyDeviceToHost));
+    const bool merged = c->comm != nullptr;
+    for (long long h = 0; h < c->n_cubes; h++) {
+      long long a = off[h], b = off[h + 1];
+      if (!merged) { a = std::max(a, s.lo); b = std::min(b, s.hi); }
+      counts[h] = b > a ? b - a : 0;
+    }
+  }
+  return VPB_OK;
+}
+
+int vpb_get_run_base(vpb_ctx *c, int64_t *run_base) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  Sched s;
+  CK(cudaMemcpy(&s, c->sched, sizeof(s), cudaMemcpyDeviceToHost));
+  *run_base = s.run_base_next;
+  return VPB_OK;
+}
+
+int vpb_set_run_base(vpb_ctx *c, int64_t run_base) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  Sched s;
+  CK(cudaMemcpy(&s, c->sched, sizeof(s), cudaMemcpyDeviceToHost));
+  s.run_base_next = run_base;
+  CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
+  return VPB_OK;
+}
+
+int vpb_iteration_host(vpb_ctx *c, const double *edges_in, double *edges_out, double *estimate,
+                       double *variance, int64_t *evals) {
+  TRY(setdev(c));
+  const size_t ne = (size_t)c->dims * (c->ng + 1);
+  if (edges_in)
+    CK(cudaMemcpyAsync(c->edges, edges_in, sizeof(double) * ne, cudaMemcpyHostToDevice, c->st));
+  const int it = c->it_enq;
+  TRY(enqueue_iteration(c));
+  if (estimate) CK(cudaMemcpyAsync(estimate, c->h_est + it, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (variance) CK(cudaMemcpyAsync(variance, c->h_var + it, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  if (evals) CK(cudaMemcpyAsync(evals, c->h_evals + it, sizeof(long long), cudaMemcpyDeviceToHost, c->st));
+  if (edges_out)
+    CK(cudaMemcpyAsync(edges_out, c->edges, sizeof(double) * ne, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  int status = 0;
+  CK(cudaMemcpy(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (status & 1) return fail(VPB_ERR_NONFINITE, "integrand returned a non-finite value");
+  if (status & 2) return fail(VPB_ERR_ASSERT, "grid update lost strict monotonicity");
+  return VPB_OK;
+}
+
+int vpb_fill(vpb_ctx *c, int64_t run_base) {
+  TRY(setdev(c));
+  CK(cudaMemcpyAsync(c->explicit_rb, &run_base, sizeof(long long), cudaMemcpyHostToDevice, c->st));
+  TRY(enqueue_plan(c, 0, c->explicit_rb));
+  TRY(enqueue_fill(c, true));
+  CK(cudaStreamSynchronize(c->st));
+  int status = 0;
+  CK(cudaMemcpy(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (status & 1) return fail(VPB_ERR_NONFINITE, "integrand returned a non-finite value");
+  if (status & 2) return fail(VPB_ERR_ASSERT, "fill failed");
+  return VPB_OK;
+}
+
+// ------------------------------------------------------ stateless parity --
+namespace {
+template <class T>
+struct DBuf {
+  T *p = nullptr;
+  ~DBuf() { if (p) cudaFree(p); }
+  int alloc(size_t n) { return dalloc(&p, n); }
+  int up(const T *h, size_t n) {
+    TRY(alloc(n));
+    if (n) CK(cudaMemcpy(p, h, sizeof(T) * n, cudaMemcpyHostToDevice));
+    return VPB_OK;
+  }
+  int down(T *h, size_t n) {
+    if (n) CK(cudaMemcpy(h, p, sizeof(T) * n, cudaMemcpyDeviceToHost));
+    return VPB_OK;
+  }
+};
+unsigned nblk(long long n, int t) { return (unsigned)std::max<long long>(1, (n + t - 1) / t); }
+}  // namespace
+
+int vpb_philox_host(const uint64_t *block, const uint64_t *stream, const uint64_t *seed, int64_t n,
+                    uint64_t *out) {
+  DBuf<uint64_t> b, s, k, o;
+  TRY(b.up(block, n)); TRY(s.up(stream, n)); TRY(k.up(seed, n)); TRY(o.alloc(2 * n));
+  philox_kernel<<<nblk(n, 256), 256>>>(b.p, s.p, k.p, n, o.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, 2 * n);
+}
+
+int vpb_uniform_at_host(const uint64_t *seed, const uint64_t *stream, const uint64_t *pos, int64_t n,
+                        double *out) {
+  DBuf<uint64_t> k, s, p;
+  DBuf<double> o;
+  TRY(k.up(seed, n)); TRY(s.up(stream, n)); TRY(p.up(pos, n)); TRY(o.alloc(n));
+  uniform_kernel<<<nblk(n, 256), 256>>>(k.p, s.p, p.p, n, o.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, n);
+}
+
+int vpb_sample_runs_host(uint64_t seed, int64_t batch, int64_t run_base, int64_t run_start,
+                         int64_t n, const int64_t *offsets, int64_t n_cubes, const double *edges,
+                         int32_t dims, int32_t ng, int64_t n_strat, double *x, double *jac,
+                         int64_t *idx, int64_t *cube) {
+  if (batch < 1 || n_strat < 1 || dims < 1 || ng < 2) return fail(VPB_ERR_INVALID, "bad geometry");
+  DBuf<long long> off, di, dc;
+  DBuf<double> de, dx, dj;
+  TRY(off.up((const long long *)offsets, n_cubes + 1));
+  TRY(de.up(edges, (size_t)dims * (ng + 1)));
+  TRY(dx.alloc((size_t)n * dims)); TRY(dj.alloc(n)); TRY(di.alloc((size_t)n * dims)); TRY(dc.alloc(n));
+  sample_runs_kernel<<<nblk(n, 128), 128>>>(seed, batch, run_base, run_start, n, off.p, n_cubes,
+                                            de.p, dims, ng, n_strat, dx.p, dj.p, di.p, dc.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  TRY(dx.down(x, (size_t)n * dims)); TRY(dj.down(jac, n));
+  TRY(di.down((long long *)idx, (size_t)n * dims)); TRY(dc.down((long long *)cube, n));
+  return VPB_OK;
+}
+
+namespace {
+template <int ID>
+__global__ void eval_kernel(const double *x, long long n, int dims, IParams P, double *out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xl[VPB_MAX_DIMS];
+  for (int j = 0; j < dims; j++) xl[j] = x[i * dims + j];
+  out[i] = integrand<ID, 0>(xl, dims, P);
+}
+}  // namespace
+
+int vpb_eval_host(int32_t id, const double *params, int32_t n_params, const double *x, int64_t n,
+                  int32_t dims, double *out) {
+  if (id < 0 || id >= VPB_N_INTEGRANDS) return fail(VPB_ERR_UNSUPPORTED, "unknown integrand id");
+  if (dims < 1 || dims > VPB_MAX_DIMS) return fail(VPB_ERR_INVALID, "bad dims");
+  IParams P{};
+  P.n = n_params;
+  for (int i = 0; i < n_params && i < VPB_MAX_PARAMS; i++) P.p[i] = params[i];
+  DBuf<double> dx, o;
+  TRY(dx.up(x, (size_t)n * dims));
+  TRY(o.alloc(n));
+  const unsigned g = nblk(n, 128);
+  switch (id) {
+#define X(I) case I: eval_kernel<I><<<g, 128>>>(dx.p, n, dims, P, o.p); break;
+    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11)
+#undef X
+  }
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, n);
+}
+
+int vpb_fill_host(const int64_t *offsets, int64_t n_cubes, const double *edges, int32_t dims,
+                  int32_t ng, int64_t n_strat, uint64_t seed, int64_t batch, int64_t run_base,
+                  int32_t integrand, const double *params, int32_t n_params, int64_t run_lo,
+                  int64_t run_hi, double *map_w, int64_t *map_counts, double *s1, double *s2,
+                  int64_t *counts, int64_t *err_run, double *err_point, double *err_value) {
+  // geometry check: n_cubes must be n_strat**dims
+  long long nc = 1;
+  for (int j = 0; j < dims; j++) nc *= n_strat;
+  if (nc != n_cubes) return fail(VPB_ERR_INVALID, "n_cubes != n_strat**dims");
+  const long long total = offsets[n_cubes];
+  if (!(0 <= run_lo && run_lo <= run_hi && run_hi <= total))
+    return fail(VPB_ERR_INVALID, "run range outside the plan");
+  std::vector<double> bnds(2 * dims);
+  for (int j = 0; j < dims; j++) {
+    bnds[2 * j] = edges[(size_t)j * (ng + 1)];
+    bnds[2 * j + 1] = edges[(size_t)j * (ng + 1) + ng];
+  }
+  vpb_desc d{};
+  d.dims = dims; d.n_intervals = ng; d.n_strat = n_strat;
+  d.n_eval = std::max<long long>(4, total);
+  d.batch_size = batch; d.seed = seed; d.alpha = 0.5; d.beta = 0.75;
+  d.integrand = integrand; d.n_params = n_params; d.params = params; d.bounds = bnds.data();
+  d.device = -1; d.max_it = 1; d.stream = nullptr;
+  vpb_ctx *c = nullptr;
+  TRY(vpb_create(&d, &c));
+  struct Guard { vpb_ctx *c; ~Guard() { vpb_destroy(c); } } guard{c};
+  TRY(vpb_set_edges(c, edges));
+  std::vector<int64_t> nh(n_cubes);
+  for (long long h = 0; h < n_cubes; h++) nh[h] = offsets[h + 1] - offsets[h];
+  // the plan kernels compute [lo, hi) from (world, rank); for an arbitrary
+  // range use a host-side schedule instead
+  CK(cudaMemcpyAsync(c->n_h, nh.data(), sizeof(long long) * n_cubes, cudaMemcpyHostToDevice, c->st));
+  nh_blocksum_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum);
+  TRY(enqueue_plan(c, 0, c->explicit_rb));
+  CK(cudaStreamSynchronize(c->st));
+  Sched s;
+  CK(cudaMemcpy(&s, c->sched, sizeof(s), cudaMemcpyDeviceToHost));
+  s.run_base = run_base;
+  s.lo = run_lo;
+  s.hi = run_hi;
+  s.ntiles = (run_hi - run_lo + FILL_TILE - 1) / FILL_TILE;
+  CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
+  // rebuild the tile table for the explicit range (block prefixes still in bsum)
+  plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,
+                                                             c->offsets, c->sched, c->tile_cube);
+  CK(cudaGetLastError());
+  TRY(enqueue_fill(c, false));
+  CK(cudaStreamSynchronize(c->st));
+  int status = 0;
+  CK(cudaMemcpy(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost));
+  if (status & 1) {
+    int64_t r;
+    double v;
+    std::vector<double> pt(dims);
+    TRY(vpb_error_info(c, &r, pt.data(), &v));
+    if (err_run) *err_run = r;
+    if (err_point) std::memcpy(err_point, pt.data(), sizeof(double) * dims);
+    if (err_value) *err_value = v;
+    return fail(VPB_ERR_NONFINITE, "integrand returned a non-finite value");
+  }
+  const size_t m = (size_t)dims * ng;
+  if (map_w) CK(cudaMemcpy(map_w, c->map_w, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  if (map_counts) CK(cudaMemcpy(map_counts, c->map_counts, sizeof(long long) * m, cudaMemcpyDeviceToHost));
+  if (s1) CK(cudaMemcpy(s1, c->s1, sizeof(double) * n_cubes, cudaMemcpyDeviceToHost));
+  if (s2) CK(cudaMemcpy(s2, c->s2, sizeof(double) * n_cubes, cudaMemcpyDeviceToHost));
+  if (counts)
+    for (long long h = 0; h < n_cubes; h++) {
+      const long long a = std::max<long long>(offsets[h], run_lo);
+      const long long b = std::min<long long>(offsets[h + 1], run_hi);
+      counts[h] = b > a ? b - a : 0;
+    }
+  return VPB_OK;
+}
+
+int vpb_pairwise_sum_host(const double *a, int64_t n, double *out) {
+  PwPlan pw;
+  pw.build(n);
+  TRY(pw.upload());
+  struct G { PwPlan *p; ~G() { p->release(); } } g{&pw};
+  DBuf<double> da, vals, o;
+  TRY(da.up(a, n)); TRY(vals.alloc(3 * (size_t)(pw.L + pw.I))); TRY(o.alloc(1));
+  array_leaf_kernel<<<nblk(pw.L, 128), 128>>>(da.p, pw.dev(), vals.p);
+  array_tree_kernel<<<1, 1024>>>(pw.dev(), vals.p, o.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, 1);
+}
+
+namespace {
+__global__ void pow_kernel(const double *x, long long n, double y, double *out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = np_scalar_pow(x[i], y);
+}
+}  // namespace
+
+int vpb_pow_host(const double *x, int64_t n, double y, double *out) {
+  DBuf<double> dx, o;
+  TRY(dx.up(x, n)); TRY(o.alloc(n));
+  pow_kernel<<<nblk(n, 256), 256>>>(dx.p, n, y, o.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, n);
+}
+
+namespace {
+// compute_results on host accumulators with explicit counts: offsets are
+// synthesised from the counts so the same kernels run.
+int results_common(const double *s1, const double *s2, const int64_t *counts, int64_t n,
+                   double beta, double *est, double *var, double *d_h, double *dp_out,
+                   double *tot_out) {
+  for (long long h = 0; h < n; h++)
+    if (counts[h] < 2) {
+      long long amin = 0;
+      for (long long k = 0; k < n; k++) if (counts[k] < counts[amin]) amin = k;
+      return fail(VPB_ERR_ASSERT, "cube " + std::to_string(amin) + " has " +
+                                      std::to_string(counts[amin]) +
+                                      " samples; every cube needs >= 2");
+    }
+  std::vector<long long> off(n + 1);
+  off[0] = 0;
+  for (long long h = 0; h < n; h++) off[h + 1] = off[h] + counts[h];
+  PwPlan pw;
+  pw.build(n);
+  TRY(pw.upload());
+  struct G { PwPlan *p; ~G() { p->release(); } } g{&pw};
+  DBuf<double> a, b, dh, dp, vals, he, hv;
+  DBuf<long long> doff, hev;
+  DBuf<Scalars> sc;
+  DBuf<Sched> sch;
+  DBuf<int> st;
+  TRY(a.up(s1, n)); TRY(b.up(s2, n)); TRY(doff.up(off.data(), n + 1));
+  TRY(dh.alloc(n)); TRY(dp.alloc(n)); TRY(vals.alloc(3 * (size_t)(pw.L + pw.I)));
+  TRY(sc.alloc(1)); TRY(sch.alloc(1)); TRY(st.alloc(1)); TRY(he.alloc(1)); TRY(hv.alloc(1));
+  CK(cudaMemset(st.p, 0, sizeof(int)));
+  CK(cudaMemset(sch.p, 0, sizeof(Sched)));
+  const double V = 1.0 / (double)n;
+  results_leaf_kernel<<<nblk(pw.L, 128), 128>>>(a.p, b.p, doff.p, n, V, beta, pw.dev(), dh.p,
+                                                dp.p, vals.p, st.p);
+  results_tree_kernel<<<1, 1024>>>(pw.dev(), vals.p, n, V, sc.p, he.p, hv.p, sch.p, st.p, 0);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  Scalars s;
+  TRY(sc.down(&s, 1));
+  if (est) *est = s.estimate;
+  if (var) *var = s.variance;
+  if (tot_out) *tot_out = s.total_dp;
+  if (d_h) TRY(dh.down(d_h, n));
+  if (dp_out && beta != 0.0) TRY(dp.down(dp_out, n));
+  return VPB_OK;
+}
+}  // namespace
+
+int vpb_compute_results_host(const double *s1, const double *s2, const int64_t *counts, int64_t n,
+                             double *estimate, double *variance, double *d_h) {
+  return results_common(s1, s2, counts, n, 0.0, estimate, variance, d_h, nullptr, nullptr);
+}
+
+int vpb_update_evals_host(const double *d_h, int64_t n, double beta, int64_t n_eval, int64_t *n_h) {
+  if (beta < 0) return fail(VPB_ERR_INVALID, "beta must be >= 0");
+  for (long long h = 0; h < n; h++)
+    if (d_h[h] < 0) return fail(VPB_ERR_INVALID, "d_h entries must be nonnegative");
+  // dp = d_h**beta and its pairwise total, on device (same kernels as the
+  // iteration: the leaf kernel applied to an identity accumulator set)
+  PwPlan pw;
+  pw.build(n);
+  TRY(pw.upload());
+  struct G { PwPlan *p; ~G() { p->release(); } } g{&pw};
+  DBuf<double> dh, dp, vals, o;
+  DBuf<long long> nh, bs;
+  DBuf<Scalars> sc;
+  DBuf<int> st;
+  TRY(dh.up(d_h, n)); TRY(dp.alloc(n)); TRY(vals.alloc(3 * (size_t)(pw.L + pw.I)));
+  TRY(nh.alloc(n)); TRY(bs.alloc((n + PLAN_NT - 1) / PLAN_NT)); TRY(sc.alloc(1)); TRY(st.alloc(1));
+  CK(cudaMemset(st.p, 0, sizeof(int)));
+  const double p = 1.0 / (double)n;
+  long long un = (long long)std::ceil((double)n_eval * p);
+  un = un < 2 ? 2 : un;
+  Scalars s{};
+  if (beta != 0.0) {
+    pow_kernel<<<nblk(n, 256), 256>>>(dh.p, n, beta, dp.p);
+    array_leaf_kernel<<<nblk(pw.L, 128), 128>>>(dp.p, pw.dev(), vals.p);
+    TRY(o.alloc(1));
+    array_tree_kernel<<<1, 1024>>>(pw.dev(), vals.p, o.p);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    TRY(o.down(&s.total_dp, 1));
+  }
+  CK(cudaMemcpy(sc.p, &s, sizeof(s), cudaMemcpyHostToDevice));
+  alloc_kernel<<<nblk(n, PLAN_NT), PLAN_NT>>>(dp.p, n, beta, (double)n_eval, un, sc.p,
+                                              beta == 0.0, nh.p, bs.p, st.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return nh.down((long long *)n_h, n);
+}
+
+int vpb_build_plan_host(const int64_t *n_h, int64_t n, int64_t *offsets) {
+  const long long nb = (n + PLAN_NT - 1) / PLAN_NT;
+  DBuf<long long> nh, bs, off, ev, rb;
+  DBuf<Sched> sch;
+  DBuf<int> st, tc;
+  TRY(nh.up((const long long *)n_h, n)); TRY(bs.alloc(nb)); TRY(off.alloc(n + 1));
+  TRY(sch.alloc(1)); TRY(st.alloc(1)); TRY(ev.alloc(1)); TRY(rb.alloc(1));
+  long long tot = 0;
+  for (long long h = 0; h < n; h++) tot += n_h[h];
+  TRY(tc.alloc(tot / FILL_TILE + 3));
+  CK(cudaMemset(st.p, 0, sizeof(int)));
+  CK(cudaMemset(sch.p, 0, sizeof(Sched)));
+  CK(cudaMemset(rb.p, 0, sizeof(long long)));
+  nh_blocksum_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p);
+  plan_scan_kernel<<<1, PLAN_NT>>>(bs.p, nb, sch.p, 1, 0, ev.p, 0, tot / FILL_TILE + 2, st.p, rb.p);
+  plan_offsets_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p, off.p, sch.p, tc.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return off.down((long long *)offsets, n + 1);
+}
+
+int vpb_smooth_and_damp_host(const double *map_w, const int64_t *map_counts, int32_t dims,
+                             int32_t ng, double alpha, double *out) {
+  if (alpha < 0) return fail(VPB_ERR_INVALID, "alpha must be >= 0");
+  const size_t m = (size_t)dims * ng;
+  DBuf<double> w, e, scr, o;
+  DBuf<long long> cnt;
+  DBuf<int> st;
+  TRY(w.up(map_w, m)); TRY(cnt.up((const long long *)map_counts, m));
+  TRY(e.alloc((size_t)dims * (ng + 1))); TRY(scr.alloc((size_t)dims * (5 * ng + 2)));
+  TRY(o.alloc(m)); TRY(st.alloc(1));
+  // uniform dummy edges; only the damped weights are returned
+  std::vector<double> he((size_t)dims * (ng + 1));
+  for (int j = 0; j < dims; j++)
+    for (int i = 0; i <= ng; i++) he[(size_t)j * (ng + 1) + i] = (double)i / ng;
+  CK(cudaMemcpy(e.p, he.data(), sizeof(double) * he.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemset(st.p, 0, sizeof(int)));
+  refine_kernel<<<dims, 256>>>(e.p, w.p, cnt.p, ng, alpha, scr.p, st.p, o.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return o.down(out, m);
+}
+
+namespace {
+// update_grid alone: feed damped weights straight into the grid stage by
+// giving the refine kernel map_w = damped, counts = 1 and alpha = 1 is NOT
+// equivalent (smoothing); use a dedicated kernel instead.
+__global__ void update_grid_kernel(double *edges, const double *damped, int ng, double *scratch,
+                                   int *status) {
+  const int j = blockIdx.x;
+  double *cum = scratch + (size_t)j * (2 * ng + 2);
+  double *ne = cum + ng + 1;
+  const double *w = damped + (size_t)j * ng;
+  double *e = edges + (size_t)j * (ng + 1);
+  __shared__ double s_tot;
+  __shared__ int s_skip;
+  if (threadIdx.x == 0) {
+    s_tot = pw_sum_rt(w, ng);
+    s_skip = !(s_tot > 0.0);
+    if (!s_skip) {
+      cum[0] = 0.0;
+      for (int i = 0; i < ng; i++) cum[i + 1] = __dadd_rn(cum[i], w[i]);
+    }
+  }
+  __syncthreads();
+  if (s_skip) return;
+  const double delta = __ddiv_rn(s_tot, (double)ng);
+  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) {
+    const double goal = __dmul_rn((double)i, delta);
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cum[mid + 1] >= goal) hi = mid; else lo = mid + 1;
+    }
+    const double frac = __ddiv_rn(__dadd_rn(goal, -cum[lo]), w[lo]);
+    ne[i] = __dadd_rn(e[lo], __dmul_rn(frac, __dadd_rn(e[lo + 1], -e[lo])));
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const double a = i == 0 ? e[0] : ne[i];
+    const double b = i == ng - 1 ? e[ng] : ne[i + 1];
+    bad |= !(b > a);
+  }
+  bad = __syncthreads_or(bad);
+  if (bad) { if (threadIdx.x == 0) atomicOr(status, 2); return; }
+  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) e[i] = ne[i];
+}
+}  // namespace
+
+int vpb_update_grid_host(const double *edges, const double *damped, int32_t dims, int32_t ng,
+                         double *out) {
+  const size_t m = (size_t)dims * ng, me = (size_t)dims * (ng + 1);
+  for (size_t i = 0; i < m; i++)
+    if (damped[i] < 0) return fail(VPB_ERR_INVALID, "damped weights must be nonnegative");
+  DBuf<double> e, w, scr;
+  DBuf<int> st;
+  TRY(e.up(edges, me)); TRY(w.up(damped, m)); TRY(scr.alloc((size_t)dims * (2 * ng + 2)));
+  TRY(st.alloc(1));
+  CK(cudaMemset(st.p, 0, sizeof(int)));
+  update_grid_kernel<<<dims, 256>>>(e.p, w.p, ng, scr.p, st.p);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  int status = 0;
+  CK(cudaMemcpy(&status, st.p, sizeof(int), cudaMemcpyDeviceToHost));
+  TRY(e.down(out, me));
+  if (status & 2) return fail(VPB_ERR_ASSERT, "grid update lost strict monotonicity");
+  return VPB_OK;
+}
+

@@ -1,0 +1,176 @@
+// devmath.cuh -- bit-exact arithmetic building blocks for the VEGAS+ hot path.
+//
+// The translation unit is compiled with -fmad=false: every plain `a*b+c` is
+// two IEEE-rounded operations, exactly like the numba/numpy reference
+// ("0 FMA").  Fused multiply-adds appear only where written
+// explicitly as __fma_rn and are then proven exact (Markstein division,
+// integer->double reconstruction) or used in functions whose reference is a
+// non-bitwise libm/SIMD transcendental (exp).
+#pragma once
+#include <cstdint>
+
+namespace vpb {
+
+// ---------------------------------------------------------------- Philox --
+// Philox4x32-10 (vp/rng.py:24-60).  Counter = (block lo, block hi, stream lo,
+// stream hi), key = (seed lo, seed hi); returns the two 64-bit output words
+// (c0<<32|c1, c2<<32|c3).  The ten round keys are hoisted into registers by
+// the caller (they depend on the seed only -> uniform across the grid).
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+  __host__ __device__ explicit PhiloxKeys(uint64_t seed) {
+    uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+      k0[r] = a; k1[r] = b;
+      a += 0x9E3779B9u; b += 0xBB67AE85u;
+    }
+  }
+};
+
+__device__ __forceinline__ void philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                       const PhiloxKeys &K, uint64_t &w0, uint64_t &w1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint64_t p0 = (uint64_t)c0 * 0xD2511F53u;   // IMAD.WIDE.U32
+    const uint64_t p1 = (uint64_t)c2 * 0xCD9E8D57u;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k0[r];   // LOP3
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k1[r];
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+  }
+  w0 = ((uint64_t)c0 << 32) | c1;
+  w1 = ((uint64_t)c2 << 32) | c3;
+}
+
+// ------------------------------------------------ uniforms and division --
+// u = (w >> 11) * 2^-53 exactly (vp/rng.py:68), in two FP64 ops instead of a
+// quarter-rate I2F.F64.U64: the low 52 bits become the mantissa of a number
+// in [1,2), and bit 52 adds 0.5.  Exhaustively argued in
+// tools/proofs/markstein_div.c (checked against (double)m * 2^-53).
+__device__ __forceinline__ double unit_from_word(uint64_t w) {
+  const uint64_t m = w >> 11;
+  const double t = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
+  const double half = (m >> 52) ? 0.5 : 0.0;
+  return __fma_rn(__dadd_rn(t, -1.0), 0.5, half);   // both steps exact
+}
+
+// RN(a / b) for b = n_strat (integer) and a = a Philox uniform or an integer
+// digit: q0 = RN(a*r), e = a - b*q0 (exact by FMA), q = RN(q0 + e*r) with
+// r = RN(1/b).  Markstein's correction; checked bitwise against IEEE
+// division for every n_strat <= 4100 (tools/proofs/markstein_div.c).
+__device__ __forceinline__ double div_exact(double a, double b, double r) {
+  const double q0 = __dmul_rn(a, r);
+  const double e = __fma_rn(-q0, b, a);
+  return __fma_rn(e, r, q0);
+}
+
+// ------------------------------------------------------------------ exp --
+// exp(x) with < 1 ulp error on the normal range, no table, branch-free:
+// k = rint(x/ln2) via the 1.5*2^52 shifter, two-step Cody-Waite reduction,
+// degree-13 Taylor/Horner on |r| <= ln2/2 (truncation < 4e-18), scaling by
+// 2^k split in two factors so underflow/overflow saturate (to 0 / inf).
+// NaN propagates (the non-finite detection of vp/executor.py:120-126 relies
+// on it).  The reference evaluates numpy's SIMD exp / libm exp, which are
+// not correctly rounded either: integrand values agree to a few ulp.
+__device__ __forceinline__ double fast_exp(double x) {
+  x = (x < -1400.0) ? -1400.0 : x;
+  x = (x > 1400.0) ? 1400.0 : x;
+  const double SH = 6755399441055744.0;   // 1.5 * 2^52
+  double kd = __fma_rn(x, 1.4426950408889634074, SH);
+  const int k = __double2loint(kd);
+  kd = __dadd_rn(kd, -SH);
+  double r = __fma_rn(kd, -6.93147180369123816490e-01, x);   // ln2 hi (trailing zeros)
+  r = __fma_rn(kd, -1.90821492927058770002e-10, r);            // ln2 lo
+  double p = 1.0 / 6227020800.0;            // 1/13!
+  p = __fma_rn(p, r, 1.0 / 479001600.0);    // 1/12!
+  p = __fma_rn(p, r, 1.0 / 39916800.0);
+  p = __fma_rn(p, r, 1.0 / 3628800.0);
+  p = __fma_rn(p, r, 1.0 / 362880.0);
+  p = __fma_rn(p, r, 1.0 / 40320.0);
+  p = __fma_rn(p, r, 1.0 / 5040.0);
+  p = __fma_rn(p, r, 1.0 / 720.0);
+  p = __fma_rn(p, r, 1.0 / 120.0);
+  p = __fma_rn(p, r, 1.0 / 24.0);
+  p = __fma_rn(p, r, 1.0 / 6.0);
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  const int k1 = k >> 1, k2 = k - k1;
+  const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
+  return __dmul_rn(__dmul_rn(p, s1), s2);
+}
+
+// ----------------------------------------------- numpy pairwise summation --
+// numpy float64 add.reduce of a contiguous row: used for
+// the integrands' `.sum(axis=1)` over a compile-time number of terms.
+template <int N>
+__device__ __forceinline__ double pw_sum(const double *a) {
+  if constexpr (N < 8) {
+    double res = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  } else if constexpr (N <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    constexpr int full = N - (N % 8);
+#pragma unroll
+    for (int i = 8; i < full; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = full; i < N; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  } else {
+    constexpr int n2 = (N / 2) - ((N / 2) % 8);
+    return __dadd_rn(pw_sum<n2>(a), pw_sum<N - n2>(a + n2));
+  }
+}
+
+// Runtime-length version (recursion unrolled with an explicit stack).
+__device__ __forceinline__ double pw_leaf(const double *a, long long n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (long long i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = a[j];
+  long long i;
+  for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ inline double pw_sum_rt(const double *a, long long n) {
+  // iterative post-order traversal of numpy's split tree
+  struct Frame { long long off, n; int state; double left; };
+  Frame st[48];
+  int sp = 0;
+  st[0] = {0, n, 0, 0.0};
+  double ret = 0.0;
+  while (sp >= 0) {
+    Frame &f = st[sp];
+    if (f.n <= 128) { ret = pw_leaf(a + f.off, f.n); sp--; continue; }
+    long long n2 = f.n / 2; n2 -= n2 % 8;
+    if (f.state == 0) { f.state = 1; st[sp + 1] = {f.off, n2, 0, 0.0}; sp++; continue; }
+    if (f.state == 1) { f.left = ret; f.state = 2; st[sp + 1] = {f.off + n2, f.n - n2, 0, 0.0}; sp++; continue; }
+    ret = __dadd_rn(f.left, ret);
+    sp--;
+  }
+  return ret;
+}
+
+}  // namespace vpb

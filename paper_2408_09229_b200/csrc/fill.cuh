@@ -1,0 +1,372 @@
+// fill.cuh -- the fused VEGAS+ fill kernel (sm_100a).
+//
+// Replaces executor.parallel_fill -> fill_shard -> kernels.sample_runs +
+// f_batch + kernels.accumulate (vp/executor.py:86-166, vp/kernels.py:36-109)
+// for one rank's run range [lo, hi) of the current plan.
+//
+// Work decomposition: a persistent grid walks tiles of TILE = NT*RPT
+// consecutive runs; each thread owns RPT consecutive runs, so a thread stays
+// inside one hypercube for long stretches and keeps the cube's running sums
+// s1 = sum(jf), s2 = sum(jf^2) in registers.  Cube sums are reduced
+// deterministically and without atomics:
+//   * a cube entirely inside one thread's runs is stored directly;
+//   * a cube spanning threads is closed by a block-wide segmented scan;
+//   * a cube spanning tiles leaves per-tile carries that fill_fixup_kernel
+//     adds in tile order.
+// Per-dimension interval histograms (MapWeights.w / .counts) live in shared
+// memory (f64 via atom.shared CAS, u32 counts via native ATOMS); each CTA
+// writes its private copy to a slice that hist_reduce_kernel sums in CTA
+// order.  Cube evaluation counts are not accumulated at all: every run of the
+// plan is evaluated exactly once, so counts[h] = n_h (within the shard).
+//
+// Bitwise contract with vp/kernels.py:36-88: the
+// Philox counter layout, u = (w>>11)*2^-53, y = RN(RN(digit/N) + RN(u/N)),
+// the y >= 1 clamp, t = RN(y*ng), iv = min(trunc t, ng-1), frac = t - iv,
+// x = RN(lo + RN(frac*dx)), jac *= RN(ng*dx), all unfused.
+#pragma once
+#include <cstdint>
+
+#include "devmath.cuh"
+#include "integrands.cuh"
+
+namespace vpb {
+
+constexpr int FILL_NT = 512;   // threads per CTA
+constexpr int FILL_RPT = 4;    // consecutive runs per thread per tile
+constexpr int FILL_TILE = FILL_NT * FILL_RPT;
+constexpr int FILL_WMAX = FILL_TILE / 2 + 4;   // cube offsets window per tile
+constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
+
+// Per-iteration schedule written by the plan kernels (device memory).
+struct Sched {
+  long long run_base;     // evaluations consumed by earlier iterations
+  long long lo, hi;       // this rank's run range of the plan
+  long long ntiles;       // ceil((hi-lo)/TILE)
+  long long total;        // plan.total
+  long long run_base_next;
+  int it;                 // 0-based iteration index being processed
+  int pad;
+};
+
+struct FillArgs {
+  const long long *offsets;     // [n_cubes+1]
+  long long n_cubes;
+  const double *edges;          // [d][ng+1]
+  int dims, ng;
+  long long n_strat;
+  double nsf, rns, ngf;         // N, RN(1/N), ng as doubles
+  long long batch;
+  unsigned long long seed;
+  long long dk, ds;             // per-grid-stride advance of (k, slot)
+  const Sched *sched;
+  const int *tile_cube;         // [ntiles+1]
+  double *s1, *s2;              // [n_cubes], zeroed by the caller
+  long long *ck_head, *ck_tail; // per tile carry keys (-1 = none)
+  double *cv_head, *cv_tail;    // per tile carry values [2*tile + {0,1}]
+  int *ct_through;              // per tile: tail chain has no root in the tile
+  double *hw_part;              // [grid][d*ng]   (smem histograms)
+  unsigned *hc_part;            // [grid][d*ng]
+  double *hw_glob;              // [d*ng] (global-atomic histograms)
+  unsigned long long *hc_glob;  // [d*ng]
+  int smem_hist;                // 1: CTA-private shared histograms
+  int *status;                  // bit0 non-finite, bit1 assert
+  unsigned long long *err_run;  // min run index with a non-finite value
+  IParams P;
+};
+
+__device__ __forceinline__ double clamp_below_one(double y) {
+  // if (y >= 1.0) y = nextafter(1, 0): y >= 0, so compare the bit patterns
+  const long long b = __double_as_longlong(y);
+  return __longlong_as_double(b < 0x3FF0000000000000ll ? b : 0x3FEFFFFFFFFFFFFFll);
+}
+
+struct SegItem {   // a partial cube segment (key < 0: none)
+  long long key;
+  double v1, v2;
+};
+
+// shared-memory layout helper (bytes)
+__host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
+                                                  int smem_hist) {
+  size_t b = 0;
+  b += (size_t)dims * (ng + 1) * sizeof(double);                       // edges
+  if (smem_hist) b += (size_t)dims * ng * (sizeof(double) + sizeof(unsigned));
+  b = (b + 15) & ~(size_t)15;
+  b += (size_t)FILL_WMAX * sizeof(long long);                          // offsets window
+  b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
+  b += (size_t)FILL_NT * (2 * sizeof(double) + sizeof(int));           // scan scratch
+  b += 32 * (2 * sizeof(double) + sizeof(int));                        // warp aggregates
+  return b;
+}
+
+template <int ID, int D>
+__global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
+  const int d = D > 0 ? D : a.dims;
+  const int ng = a.ng;
+  const int tid = threadIdx.x;
+
+  // ---- shared memory carve-up
+  double *s_edges = reinterpret_cast<double *>(smem_raw);
+  size_t off = (size_t)d * (ng + 1) * sizeof(double);
+  double *s_hw = nullptr;
+  unsigned *s_hc = nullptr;
+  if (a.smem_hist) {
+    s_hw = reinterpret_cast<double *>(smem_raw + off);
+    off += (size_t)d * ng * sizeof(double);
+    s_hc = reinterpret_cast<unsigned *>(smem_raw + off);
+    off += (size_t)d * ng * sizeof(unsigned);
+  }
+  off = (off + 15) & ~(size_t)15;
+  long long *s_win = reinterpret_cast<long long *>(smem_raw + off);
+  off += (size_t)FILL_WMAX * sizeof(long long);
+  const bool dq_tab = a.n_strat <= DQ_TABLE_MAX;
+  double *s_dq = reinterpret_cast<double *>(smem_raw + off);
+  off += (dq_tab ? (size_t)a.n_strat : 0) * sizeof(double);
+  double *s_sc1 = reinterpret_cast<double *>(smem_raw + off);
+  off += FILL_NT * sizeof(double);
+  double *s_sc2 = reinterpret_cast<double *>(smem_raw + off);
+  off += FILL_NT * sizeof(double);
+  int *s_scf = reinterpret_cast<int *>(smem_raw + off);
+  off += FILL_NT * sizeof(int);
+  double *s_w1 = reinterpret_cast<double *>(smem_raw + off);
+  off += 32 * sizeof(double);
+  double *s_w2 = reinterpret_cast<double *>(smem_raw + off);
+  off += 32 * sizeof(double);
+  int *s_wf = reinterpret_cast<int *>(smem_raw + off);
+
+  for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
+  if (a.smem_hist)
+    for (int i = tid; i < d * ng; i += FILL_NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
+  if (dq_tab)
+    for (int i = tid; i < a.n_strat; i += FILL_NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
+
+  const Sched S = *a.sched;
+  const PhiloxKeys K(a.seed);
+  const long long lo = S.lo, hi = S.hi, ntiles = S.ntiles;
+  const unsigned long long batch = (unsigned long long)a.batch;
+  const unsigned long long stride_half = (unsigned long long)((d + (d & 1)) >> 1);
+  __syncthreads();
+
+  // (k, slot) of this thread's first run in its first tile; advanced per grid stride
+  unsigned long long g0 = (unsigned long long)(S.run_base + lo + (long long)blockIdx.x * FILL_TILE +
+                                               (long long)tid * FILL_RPT);
+  unsigned long long kk = g0 / batch, slot = g0 % batch;
+
+  const int lane = tid & 31, warp = tid >> 5;
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long T0 = lo + tile * FILL_TILE;
+    const long long T1 = min(T0 + (long long)FILL_TILE, hi);
+    const long long c_first = a.tile_cube[tile];
+    const long long c_last = a.tile_cube[tile + 1];
+    const int nwin = (int)(c_last - c_first + 2);
+    for (int i = tid; i < nwin; i += FILL_NT) s_win[i] = a.offsets[c_first + i];
+    // no head carry unless a thread below publishes one (after the barriers)
+    if (tid == 0) a.ck_head[tile] = -1;
+    __syncthreads();
+
+    const long long r0 = T0 + (long long)tid * FILL_RPT;
+    const long long r1 = min(r0 + (long long)FILL_RPT, T1);
+    SegItem H{-1, 0.0, 0.0}, T{-1, 0.0, 0.0};
+    int t_through = 0;
+
+    if (r0 < r1) {
+      // cube of r0: largest i with win[i] <= r0
+      int lo_i = 0, hi_i = nwin - 2;
+      while (lo_i < hi_i) {
+        const int mid = (lo_i + hi_i + 1) >> 1;
+        if (s_win[mid] <= r0) lo_i = mid; else hi_i = mid - 1;
+      }
+      int wi = lo_i;
+      long long cube = c_first + wi;
+      long long cube_beg = s_win[wi], cube_end = s_win[wi + 1];
+      long long seg_beg = r0;
+      double v1 = 0.0, v2 = 0.0;
+      unsigned long long k = kk, sl = slot;
+      double dq[MAXD];
+      auto load_digits = [&](long long c) {
+        long long rem = c;
+#pragma unroll
+        for (int j = 0; j < (D > 0 ? D : d); j++) {
+          const long long q = rem / a.n_strat;
+          const long long dig = rem - q * a.n_strat;
+          rem = q;
+          dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
+        }
+      };
+      auto close_segment = [&](long long seg_end) {
+        const bool before = cube_beg < seg_beg;   // cube started before this thread
+        const bool after = cube_end > seg_end;    // cube continues past this thread
+        if (!before && !after) {
+          a.s1[cube] = v1;
+          a.s2[cube] = v2;
+        } else if (before && !after) {
+          H = {cube, v1, v2};
+        } else {
+          T = {cube, v1, v2};
+          t_through = before ? 1 : 0;
+        }
+      };
+      load_digits(cube);
+      for (long long r = r0; r < r1; r++) {
+        if (r >= cube_end) {
+          close_segment(r);
+          do { wi++; } while (s_win[wi + 1] <= r);
+          cube = c_first + wi;
+          cube_beg = s_win[wi];
+          cube_end = s_win[wi + 1];
+          seg_beg = r;
+          v1 = 0.0; v2 = 0.0;
+          load_digits(cube);
+        }
+        // ---- sample (vp/kernels.py:59-88)
+        const unsigned long long base = k * stride_half;
+        double x[MAXD];
+        int iv[MAXD];
+        double jac = 1.0;
+        uint64_t w0 = 0, w1 = 0;
+#pragma unroll
+        for (int j = 0; j < (D > 0 ? D : d); j++) {
+          if ((j & 1) == 0) {
+            const unsigned long long blk = base + (unsigned long long)(j >> 1);
+            philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+                   w0, w1);
+          }
+          const double u = unit_from_word((j & 1) ? w1 : w0);
+          const double y = clamp_below_one(__dadd_rn(dq[j], div_exact(u, a.nsf, a.rns)));
+          const double t = __dmul_rn(y, a.ngf);
+          // trunc(t) for 0 <= t < 2^31 via the 2^52 shifter in round-toward-zero
+          const double sh = __dadd_rz(t, 4503599627370496.0);
+          int ivj = __double2loint(sh);
+          double frac = __dadd_rn(t, -__dadd_rn(sh, -4503599627370496.0));
+          if (ivj > ng - 1) {   // t rounded up to ng (y = 1 - 2^-53)
+            ivj = ng - 1;
+            frac = __dadd_rn(t, -(double)(ng - 1));
+          }
+          const double *e = s_edges + j * (ng + 1) + ivj;
+          const double elo = e[0];
+          const double dx = __dadd_rn(e[1], -elo);
+          x[j] = __dadd_rn(elo, __dmul_rn(frac, dx));
+          jac = __dmul_rn(jac, __dmul_rn(a.ngf, dx));
+          iv[j] = ivj;
+        }
+        // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
+        const double f = integrand<ID, D>(x, d, a.P);
+        if (!isfinite(f)) {
+          atomicMin(a.err_run, (unsigned long long)r);
+          atomicOr(a.status, 1);
+        } else {
+          const double jf = __dmul_rn(jac, f);
+          const double w2 = __dmul_rn(jf, jf);
+          v1 = __dadd_rn(v1, jf);
+          v2 = __dadd_rn(v2, w2);
+          // ---- interval histograms (vp/kernels.py:100-105)
+          if (a.smem_hist) {
+#pragma unroll
+            for (int j = 0; j < (D > 0 ? D : d); j++) {
+              atomicAdd(&s_hw[j * ng + iv[j]], w2);
+              atomicAdd(&s_hc[j * ng + iv[j]], 1u);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < (D > 0 ? D : d); j++) {
+              atomicAdd(&a.hw_glob[j * ng + iv[j]], w2);
+              atomicAdd(&a.hc_glob[j * ng + iv[j]], 1ull);
+            }
+          }
+        }
+        if (++sl == batch) { sl = 0; k++; }
+      }
+      close_segment(r1);
+    }
+
+    // ---- block segmented scan of the tail items (chain values flow forward)
+    // element: (flag = chain restarts here, v); flag=1 also for "no tail".
+    int fl = (T.key < 0) ? 1 : (t_through ? 0 : 1);
+    double e1 = T.key < 0 ? 0.0 : T.v1, e2 = T.key < 0 ? 0.0 : T.v2;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int pf = __shfl_up_sync(0xffffffffu, fl, o);
+      const double p1 = __shfl_up_sync(0xffffffffu, e1, o);
+      const double p2 = __shfl_up_sync(0xffffffffu, e2, o);
+      if (lane >= o && !fl) { e1 = __dadd_rn(p1, e1); e2 = __dadd_rn(p2, e2); }
+      if (lane >= o) fl |= pf;
+    }
+    if (lane == 31) { s_w1[warp] = e1; s_w2[warp] = e2; s_wf[warp] = fl; }
+    __syncthreads();
+    if (warp == 0) {
+      constexpr int NW = FILL_NT / 32;
+      int wf = lane < NW ? s_wf[lane] : 1;
+      double a1 = lane < NW ? s_w1[lane] : 0.0, a2 = lane < NW ? s_w2[lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int pf = __shfl_up_sync(0xffffffffu, wf, o);
+        const double p1 = __shfl_up_sync(0xffffffffu, a1, o);
+        const double p2 = __shfl_up_sync(0xffffffffu, a2, o);
+        if (lane >= o && !wf) { a1 = __dadd_rn(p1, a1); a2 = __dadd_rn(p2, a2); }
+        if (lane >= o) wf |= pf;
+      }
+      if (lane < NW) { s_w1[lane] = a1; s_w2[lane] = a2; s_wf[lane] = wf; }
+    }
+    __syncthreads();
+    // rooted: does the inclusive chain of this thread contain a restart inside the tile?
+    int rooted = fl;
+    if (warp > 0 && !fl) {
+      e1 = __dadd_rn(s_w1[warp - 1], e1);
+      e2 = __dadd_rn(s_w2[warp - 1], e2);
+      rooted = s_wf[warp - 1];
+    }
+    s_sc1[tid] = e1;
+    s_sc2[tid] = e2;
+    s_scf[tid] = rooted;
+    __syncthreads();
+    // ---- heads close chains
+    if (H.key >= 0) {
+      if (tid == 0) {
+        a.ck_head[tile] = H.key;
+        a.cv_head[2 * tile] = H.v1;
+        a.cv_head[2 * tile + 1] = H.v2;
+      } else {
+        const double t1 = __dadd_rn(s_sc1[tid - 1], H.v1);
+        const double t2 = __dadd_rn(s_sc2[tid - 1], H.v2);
+        if (s_scf[tid - 1]) {
+          a.s1[H.key] = t1;
+          a.s2[H.key] = t2;
+        } else {
+          a.ck_head[tile] = H.key;
+          a.cv_head[2 * tile] = t1;
+          a.cv_head[2 * tile + 1] = t2;
+        }
+      }
+    }
+    // ---- the tile's last thread with runs publishes the tail carry
+    const int last = (int)((T1 - T0 + FILL_RPT - 1) / FILL_RPT) - 1;
+    if (tid == last) {
+      if (T.key >= 0) {
+        a.ck_tail[tile] = T.key;
+        a.cv_tail[2 * tile] = e1;
+        a.cv_tail[2 * tile + 1] = e2;
+        a.ct_through[tile] = rooted ? 0 : 1;
+      } else {
+        a.ck_tail[tile] = -1;
+        a.ct_through[tile] = 0;
+      }
+    }
+    // advance this thread's RNG coordinates by one grid stride of tiles
+    kk += (unsigned long long)a.dk;
+    slot += (unsigned long long)a.ds;
+    if (slot >= batch) { slot -= batch; kk++; }
+    __syncthreads();   // s_win / scan scratch reused by the next tile
+  }
+
+  if (a.smem_hist) {
+    __syncthreads();
+    double *hw = a.hw_part + (size_t)blockIdx.x * d * ng;
+    unsigned *hc = a.hc_part + (size_t)blockIdx.x * d * ng;
+    for (int i = tid; i < d * ng; i += FILL_NT) { hw[i] = s_hw[i]; hc[i] = s_hc[i]; }
+  }
+}
+
+}  // namespace vpb

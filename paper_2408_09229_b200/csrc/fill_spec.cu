@@ -1,0 +1,66 @@
+// fill_spec.cu -- compile-time-dims instantiations of the fused fill kernel
+// for the registry integrands at their registry dimension and the BASELINE
+// configurations (cfg1/3: d=4, cfg2: d=8, cfg4: d=6, cfg5: d=20).
+#include "fill_launch.h"
+
+namespace vpb {
+
+namespace {
+template <int ID, int D>
+cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  fill_kernel<ID, D><<<grid, FILL_NT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+template <int ID, int D>
+cudaError_t occ_one(size_t smem, int *ctas) {
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D>, FILL_NT, smem);
+}
+}  // namespace
+
+#define VPB_SPEC_LIST(X)          \
+  X(VPB_GAUSSIAN, 4)              \
+  X(VPB_GAUSSIAN, 20)             \
+  X(VPB_RIDGE, 4)                 \
+  X(VPB_MULTIPEAK, 8)             \
+  X(VPB_GENZ_OSCILLATORY, 6)      \
+  X(VPB_GENZ_PRODUCTPEAK, 6)      \
+  X(VPB_SINEXP, 2)                \
+  X(VPB_LINEAR, 10)               \
+  X(VPB_COSINE, 10)               \
+  X(VPB_EXPONENTIAL, 10)          \
+  X(VPB_ROOS_ARNOLD, 10)          \
+  X(VPB_MOROKOFF, 8)
+
+int fill_is_specialised(int id, int dims) {
+#define X(I, D) if (id == I && dims == D) return 1;
+  VPB_SPEC_LIST(X)
+#undef X
+  return 0;
+}
+
+cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
+                        const FillArgs &a) {
+#define X(I, D) if (id == I && dims == D) return launch_one<I, D>(grid, smem, st, a);
+  VPB_SPEC_LIST(X)
+#undef X
+  return launch_fill_generic(id, grid, smem, st, a);
+}
+
+cudaError_t fill_occupancy(int id, int dims, size_t smem, int *ctas) {
+#define X(I, D) if (id == I && dims == D) return occ_one<I, D>(smem, ctas);
+  VPB_SPEC_LIST(X)
+#undef X
+  return fill_occupancy_generic(id, smem, ctas);
+}
+
+}  // namespace vpb

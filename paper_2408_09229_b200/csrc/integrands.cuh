@@ -1,0 +1,158 @@
+// integrands.cuh -- device functors for the registry integrands.
+//
+// Registry: vp/integrands.py:106-190 (sinexp, linear, cosine, exponential,
+// roos_arnold, morokoff, gaussian, ridge) plus the BASELINE-pinned synthetic
+// integrands (multipeak8 = cfg2, genz oscillatory / product-peak = cfg4,
+// gaussian20 = cfg5; definitions in paper_2408_09229_b200/integrands.py).
+// Operation order follows the reference's numpy expressions (row sums use
+// numpy's pairwise tree, products reduce left to right); exp/cos/sin are
+// device implementations, so values agree with numpy to a few ulp.
+#pragma once
+#include "devmath.cuh"
+#include "../../include/vegas_b200.h"
+
+namespace vpb {
+
+struct IParams {
+  double p[VPB_MAX_PARAMS];
+  int n;
+};
+
+// row sum with numpy's pairwise association (compile-time or runtime length)
+template <int D>
+__device__ __forceinline__ double row_sum(const double *t, int d) {
+  if constexpr (D > 0) return pw_sum<D>(t);
+  else return pw_sum_rt(t, d);
+}
+
+// 4-element sort (ridge sums run over sorted coordinates, vp/integrands.py:174-179)
+__device__ __forceinline__ void cswap(double &a, double &b) {
+  const double lo = fmin(a, b), hi = fmax(a, b);
+  a = lo; b = hi;
+}
+
+template <int ID, int D>
+__device__ __forceinline__ double integrand(const double *x, int d, const IParams &P) {
+  constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
+  if constexpr (ID == VPB_GAUSSIAN) {
+    // norm * exp(-sum((x-mu)^2) / (2 sigma^2))           vp/integrands.py:135-139
+    double t[MAXD];
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      const double u = __dadd_rn(x[j], -P.p[0]);
+      t[j] = __dmul_rn(u, u);
+    }
+    const double r2 = row_sum<D>(t, d);
+    return __dmul_rn(P.p[2], fast_exp(-__ddiv_rn(r2, P.p[3])));
+  } else if constexpr (ID == VPB_MULTIPEAK) {
+    // (1/3) sum_k norm * exp(-|x - mu_k|^2 / (2 sigma^2))
+    const int np = (int)P.p[0];
+    double out = 0.0;
+    for (int k = 0; k < np; k++) {
+      double t[MAXD];
+#pragma unroll
+      for (int j = 0; j < (D > 0 ? D : d); j++) {
+        const double u = __dadd_rn(x[j], -P.p[5 + k]);
+        t[j] = __dmul_rn(u, u);
+      }
+      const double r2 = row_sum<D>(t, d);
+      out = __dadd_rn(out, __dmul_rn(P.p[2], fast_exp(-__ddiv_rn(r2, P.p[3]))));
+    }
+    return __ddiv_rn(out, P.p[4]);
+  } else if constexpr (ID == VPB_RIDGE) {
+    // windowed sum over the 1000 diagonal centres        vp/integrands.py:154-182
+    double xs[MAXD];
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      xs[j] = x[j];
+    }
+    if constexpr (D == 4) {
+      cswap(xs[0], xs[1]); cswap(xs[2], xs[3]);
+      cswap(xs[0], xs[2]); cswap(xs[1], xs[3]);
+      cswap(xs[1], xs[2]);
+    } else {
+      for (int i = 1; i < d; i++) {
+        const double v = xs[i];
+        int j = i - 1;
+        while (j >= 0 && xs[j] > v) { xs[j + 1] = xs[j]; j--; }
+        xs[j + 1] = v;
+      }
+    }
+    double sq[MAXD];
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      sq[j] = __dmul_rn(xs[j], xs[j]);
+    }
+    const double s1 = row_sum<D>(xs, d);
+    const double s2 = row_sum<D>(sq, d);
+    const int n_cent = (int)P.p[0];
+    const double spacing = (double)n_cent - 1.0;
+    const double mu = __dmul_rn(0.25, s1);
+    const double q0 = __dadd_rn(s2, -__dmul_rn(mu, s1));
+    int lo = (int)ceil(__dmul_rn(__dadd_rn(mu, -P.p[2]), spacing));
+    int hi = (int)floor(__dmul_rn(__dadd_rn(mu, P.p[2]), spacing));
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > n_cent - 1 ? n_cent - 1 : hi;
+    const double rsp = 1.0 / spacing;
+    double acc = 0.0;
+    for (int i = lo; i <= hi; i++) {
+      const double dc = __dadd_rn(div_exact((double)i, spacing, rsp), -mu);
+      acc = __dadd_rn(acc, fast_exp(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
+    }
+    return __dmul_rn(__dmul_rn(P.p[1], fast_exp(__dmul_rn(-100.0, q0))), acc);
+  } else if constexpr (ID == VPB_GENZ_OSCILLATORY) {
+    // cos(2 pi u_1 + a . x)
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      s = __dadd_rn(s, __dmul_rn(x[j], P.p[1 + j]));
+    }
+    return cos(__dadd_rn(P.p[0], s));
+  } else if constexpr (ID == VPB_GENZ_PRODUCTPEAK) {
+    // prod_j 1 / (a_j^-2 + (x_j - u_j)^2)
+    double prod = 1.0;
+    const int dd = D > 0 ? D : d;
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      const double u = __dadd_rn(x[j], -P.p[dd + j]);
+      prod = __dmul_rn(prod, __drcp_rn(__dadd_rn(P.p[j], __dmul_rn(u, u))));
+    }
+    return prod;
+  } else if constexpr (ID == VPB_SINEXP) {
+    return __dadd_rn(sin(x[0]), fast_exp(x[1]));   // vp/integrands.py:106-107
+  } else if constexpr (ID == VPB_LINEAR) {
+    return row_sum<D>(x, d);                        // vp/integrands.py:110-111
+  } else if constexpr (ID == VPB_COSINE) {
+    double prod = cos(x[0]);                        // vp/integrands.py:114-115
+#pragma unroll
+    for (int j = 1; j < (D > 0 ? D : d); j++) {
+      prod = __dmul_rn(prod, cos(x[j]));
+    }
+    return prod;
+  } else if constexpr (ID == VPB_EXPONENTIAL) {
+    double t[MAXD];                                 // vp/integrands.py:118-119
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      t[j] = __dmul_rn(x[j], x[j]);
+    }
+    return fast_exp(row_sum<D>(t, d));
+  } else if constexpr (ID == VPB_ROOS_ARNOLD) {
+    double prod = fabs(__dadd_rn(__dmul_rn(4.0, x[0]), -2.0));   // vp/integrands.py:122-123
+#pragma unroll
+    for (int j = 1; j < (D > 0 ? D : d); j++) {
+      prod = __dmul_rn(prod, fabs(__dadd_rn(__dmul_rn(4.0, x[j]), -2.0)));
+    }
+    return prod;
+  } else if constexpr (ID == VPB_MOROKOFF) {
+    double prod = pow(x[0], P.p[1]);                // vp/integrands.py:126-128
+#pragma unroll
+    for (int j = 1; j < (D > 0 ? D : d); j++) {
+      prod = __dmul_rn(prod, pow(x[j], P.p[1]));
+    }
+    return __dmul_rn(P.p[0], prod);
+  } else {
+    return P.p[0];   // VPB_CONSTANT
+  }
+}
+
+}  // namespace vpb

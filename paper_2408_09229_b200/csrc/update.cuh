@@ -1,0 +1,507 @@
+// update.cuh -- plan, results, allocation and refinement kernels.
+//
+//   strat.build_run_plan          vp/strat.py:131-137   alloc/scan/offsets kernels
+//   strat.compute_results         vp/strat.py:183-208   results_leaf + pw_tree kernels
+//   strat.update_evals_per_cube   vp/strat.py:88-113    results_leaf (pow) + alloc kernel
+//   maps.smooth_and_damp          vp/maps.py:160-199    refine_kernel
+//   maps.update_grid              vp/maps.py:202-234    refine_kernel
+//
+// All of them are deterministic and atomic-free, so every rank computes the
+// same replicated update from the all-reduced accumulators.  numpy's pairwise
+// summation tree is reproduced exactly: the host builds the
+// tree for a given length once (PwPlan in capi.cu); leaves run in parallel,
+// inner nodes combine level by level in one CTA.
+#pragma once
+#include <cstdint>
+
+#include "devmath.cuh"
+#include "fill.cuh"
+
+namespace vpb {
+
+struct PwPlanDev {
+  const long long *leaf_off;   // [L]
+  const int *leaf_len;         // [L]
+  const int *node_l, *node_r;  // [I] children ids (leaves 0..L-1, inner L..)
+  const int *level_start;      // [H+1] inner nodes grouped by height
+  int L, I, H;
+};
+
+// numpy's `array ** scalar` fast paths, else pow.
+__device__ __forceinline__ double np_scalar_pow(double x, double e) {
+  if (e == 1.0) return x;
+  if (e == 2.0) return __dmul_rn(x, x);
+  if (e == 0.5) return __dsqrt_rn(x);
+  if (e == 0.0) return 1.0;
+  return pow(x, e);
+}
+
+// ---------------------------------------------------------------- results --
+// One thread per pairwise leaf over the cubes.  Per cube (vp/strat.py:199-207):
+//   c = n_h (every planned run was evaluated once), m = s1/c,
+//   rv = max(s2/c - m*m, 0), d_h = sqrt(rv)*V, and for the allocation
+//   dp = d_h**beta.  Leaf partial sums of m, rv/c and dp follow numpy's
+//   8-accumulator leaf exactly.
+__global__ void results_leaf_kernel(const double *s1, const double *s2, const long long *offsets,
+                                    long long n, double V, double beta, PwPlanDev pw,
+                                    double *d_h, double *dp, double *vals, const int *status) {
+  const int leaf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= pw.L || (*status & 1)) return;
+  const long long o = pw.leaf_off[leaf];
+  const int len = pw.leaf_len[leaf];
+  const bool want_dp = beta != 0.0;
+  auto elem = [&](long long h, double &m, double &t, double &p) {
+    const double c = (double)(offsets[h + 1] - offsets[h]);
+    m = __ddiv_rn(s1[h], c);
+    double rv = __dadd_rn(__ddiv_rn(s2[h], c), -__dmul_rn(m, m));
+    rv = (rv < 0.0) ? 0.0 : rv;   // np.maximum(rv, 0) keeps NaN
+    t = __ddiv_rn(rv, c);
+    const double dh = __dmul_rn(__dsqrt_rn(rv), V);
+    d_h[h] = dh;
+    p = want_dp ? np_scalar_pow(dh, beta) : 0.0;
+    if (want_dp) dp[h] = p;
+  };
+  double sm, st, sp;
+  if (len < 8) {
+    sm = 0.0; st = 0.0; sp = 0.0;
+    for (int i = 0; i < len; i++) {
+      double m, t, p;
+      elem(o + i, m, t, p);
+      sm = __dadd_rn(sm, m); st = __dadd_rn(st, t); sp = __dadd_rn(sp, p);
+    }
+  } else {
+    double rm[8], rt[8], rp[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) elem(o + j, rm[j], rt[j], rp[j]);
+    int i;
+    for (i = 8; i < len - (len % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        double m, t, p;
+        elem(o + i + j, m, t, p);
+        rm[j] = __dadd_rn(rm[j], m); rt[j] = __dadd_rn(rt[j], t); rp[j] = __dadd_rn(rp[j], p);
+      }
+    }
+    auto tree8 = [](const double *r) {
+      return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    };
+    sm = tree8(rm); st = tree8(rt); sp = tree8(rp);
+    for (; i < len; i++) {
+      double m, t, p;
+      elem(o + i, m, t, p);
+      sm = __dadd_rn(sm, m); st = __dadd_rn(st, t); sp = __dadd_rn(sp, p);
+    }
+  }
+  vals[3 * leaf + 0] = sm;
+  vals[3 * leaf + 1] = st;
+  vals[3 * leaf + 2] = sp;
+}
+
+// Generic leaf kernel for a plain array (parity entry point vpb_pairwise_sum).
+__global__ void array_leaf_kernel(const double *a, PwPlanDev pw, double *vals) {
+  const int leaf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (leaf >= pw.L) return;
+  vals[3 * leaf] = pw_leaf(a + pw.leaf_off[leaf], pw.leaf_len[leaf]);
+  vals[3 * leaf + 1] = 0.0;
+  vals[3 * leaf + 2] = 0.0;
+}
+
+// Inner nodes of the pairwise tree, by height, one CTA; three sums at once.
+__device__ void pw_tree_combine(PwPlanDev pw, double *vals) {
+  for (int h = 0; h < pw.H; h++) {
+    for (int i = pw.level_start[h] + threadIdx.x; i < pw.level_start[h + 1]; i += blockDim.x) {
+      const int l = pw.node_l[i], r = pw.node_r[i], me = pw.L + i;
+#pragma unroll
+      for (int c = 0; c < 3; c++) vals[3 * me + c] = __dadd_rn(vals[3 * l + c], vals[3 * r + c]);
+    }
+    __syncthreads();
+  }
+}
+
+struct Scalars {
+  double estimate, variance, total_dp;
+  int valid;
+};
+
+// Finishes compute_results (vp/strat.py:205-207) and records the history.
+__global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, double V,
+                                    Scalars *sc, double *hist_est, double *hist_var,
+                                    Sched *sched, const int *status, int record) {
+  if (*status & 1) return;
+  pw_tree_combine(pw, vals);
+  if (threadIdx.x == 0) {
+    const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
+    const double sm = vals[3 * root], st = vals[3 * root + 1], sp = vals[3 * root + 2];
+    sc->estimate = __ddiv_rn(sm, (double)n);
+    sc->variance = __dmul_rn(__dmul_rn(st, V), V);
+    sc->total_dp = sp;
+    sc->valid = 1;
+    if (record) {
+      hist_est[sched->it] = sc->estimate;
+      hist_var[sched->it] = sc->variance;
+    }
+  }
+}
+
+__global__ void array_tree_kernel(PwPlanDev pw, double *vals, double *out) {
+  pw_tree_combine(pw, vals);
+  if (threadIdx.x == 0) *out = vals[3 * (pw.I > 0 ? pw.L + pw.I - 1 : 0)];
+}
+
+// -------------------------------------------------------------- allocation --
+// n_h = max(ceil(n_eval * (dp/total)), 2), or the uniform share when beta == 0
+// or total <= 0 (vp/strat.py:101-113).  Also the per-block sums for the plan.
+constexpr int PLAN_NT = 1024;
+
+__global__ void alloc_kernel(const double *dp, long long n, double beta, double ne,
+                             long long uniform_nh, const Scalars *sc, int use_uniform,
+                             long long *n_h, long long *bsum, const int *status) {
+  __shared__ long long red[PLAN_NT / 32];
+  if (*status & 1) return;
+  const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
+  long long v = 0;
+  if (h < n) {
+    const double tot = sc->total_dp;
+    if (use_uniform || beta == 0.0 || !(tot > 0.0)) {
+      v = uniform_nh;
+    } else {
+      v = (long long)ceil(__dmul_rn(ne, __ddiv_rn(dp[h], tot)));
+      v = v < 2 ? 2 : v;
+    }
+    n_h[h] = v;
+  }
+  long long s = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+  }
+}
+
+// Block sums of a host-provided n_h (vpb_set_allocation).
+__global__ void nh_blocksum_kernel(const long long *n_h, long long n, long long *bsum) {
+  __shared__ long long red[PLAN_NT / 32];
+  const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
+  long long s = h < n ? n_h[h] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+  }
+}
+
+// Exclusive scan of the block sums; total; this rank's shard of the run
+// range (vp/executor.py:41-57: the first total % world ranks get +1); run_base
+// bookkeeping (vp/core.py:208) and the evals history.
+__global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, int world, int rank,
+                                 long long *hist_evals, int record, long long ntiles_cap,
+                                 int *status, const long long *explicit_run_base) {
+  __shared__ long long buf[PLAN_NT];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (long long b0 = 0; b0 < nb; b0 += PLAN_NT) {
+    const long long i = b0 + threadIdx.x;
+    const long long v = i < nb ? bsum[i] : 0;
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < PLAN_NT; o <<= 1) {
+      const long long t = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
+      __syncthreads();
+      buf[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < nb) bsum[i] = carry + buf[threadIdx.x] - v;   // exclusive
+    __syncthreads();
+    if (threadIdx.x == 0) carry += buf[PLAN_NT - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const long long total = carry;
+    Sched s = *sched;
+    if (explicit_run_base) {
+      s.run_base = *explicit_run_base;
+    } else {
+      s.run_base = s.run_base_next;
+      s.run_base_next = s.run_base + total;
+    }
+    s.total = total;
+    const long long q = total / world, rem = total % world;
+    s.lo = rank * q + (rank < rem ? rank : rem);
+    s.hi = s.lo + q + (rank < rem ? 1 : 0);
+    s.ntiles = (s.hi - s.lo + FILL_TILE - 1) / FILL_TILE;
+    if (s.ntiles > ntiles_cap) { atomicOr(status, 2); s.ntiles = 0; }
+    *sched = s;
+    if (record) hist_evals[s.it] = total;
+  }
+}
+
+// offsets[h] = exclusive prefix of n_h; tile -> first cube table for the fill.
+__global__ void plan_offsets_kernel(const long long *n_h, long long n, const long long *bpre,
+                                    long long *offsets, const Sched *sched, int *tile_cube) {
+  __shared__ long long buf[PLAN_NT];
+  const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
+  const long long v = h < n ? n_h[h] : 0;
+  buf[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < PLAN_NT; o <<= 1) {
+    const long long t = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
+    __syncthreads();
+    buf[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (h >= n) return;
+  const long long beg = bpre[blockIdx.x] + buf[threadIdx.x] - v;
+  const long long end = beg + v;
+  offsets[h] = beg;
+  if (h == n - 1) offsets[n] = end;
+  const long long lo = sched->lo, hi = sched->hi, nt = sched->ntiles;
+  const long long a = beg > lo ? beg : lo, b = end < hi ? end : hi;
+  if (a < b) {
+    // tiles whose first run lies in [a, b)
+    long long t0 = (a - lo + FILL_TILE - 1) / FILL_TILE;
+    const long long t1 = (b - lo + FILL_TILE - 1) / FILL_TILE;
+    for (long long t = t0; t < t1; t++) tile_cube[t] = (int)h;
+    if (b == hi) tile_cube[nt] = (int)h;   // sentinel: cube of the last run
+  }
+}
+
+__global__ void set_iteration_kernel(Sched *sched, int it) { sched->it = it; }
+
+// ----------------------------------------------------------------- fill ----
+// Cube chains spanning tiles, in tile order (deterministic).
+__global__ void fill_fixup_kernel(FillArgs a) {
+  const long long nt = a.sched->ntiles;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const long long key = a.ck_tail[t];
+  if (t == 0 && a.ck_head[0] >= 0) {   // cube begun before this shard
+    a.s1[a.ck_head[0]] = a.cv_head[0];
+    a.s2[a.ck_head[0]] = a.cv_head[1];
+  }
+  if (key < 0) return;
+  if (a.ct_through[t] && t != 0) return;   // continuation, owned by an earlier tile
+  double v1 = a.cv_tail[2 * t], v2 = a.cv_tail[2 * t + 1];
+  long long u = t + 1;
+  for (; u < nt; u++) {
+    if (a.ck_tail[u] == key && a.ct_through[u]) {
+      v1 = __dadd_rn(v1, a.cv_tail[2 * u]);
+      v2 = __dadd_rn(v2, a.cv_tail[2 * u + 1]);
+      continue;
+    }
+    if (a.ck_head[u] == key) {
+      v1 = __dadd_rn(v1, a.cv_head[2 * u]);
+      v2 = __dadd_rn(v2, a.cv_head[2 * u + 1]);
+    }
+    break;
+  }
+  a.s1[key] = v1;
+  a.s2[key] = v2;
+}
+
+// Sum the per-CTA histogram slices in CTA order.
+__global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
+                                   long long m, double *map_w, long long *map_counts) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double w = 0.0;
+  long long c = 0;
+  for (int b = 0; b < nparts; b++) {
+    w = __dadd_rn(w, hw_part[(size_t)b * m + i]);
+    c += hc_part[(size_t)b * m + i];
+  }
+  map_w[i] = w;
+  map_counts[i] = c;
+}
+
+__global__ void hist_glob_convert_kernel(const unsigned long long *hc, long long m,
+                                         long long *map_counts) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) map_counts[i] = (long long)hc[i];
+}
+
+// --------------------------------------------------------------- refine ----
+// One CTA per dimension: smooth_and_damp (vp/maps.py:160-199) then
+// update_grid (vp/maps.py:202-234).  Sequential steps (numpy's pairwise sum
+// and the sequential cumsum) run on one thread to keep numpy's rounding.
+__global__ void refine_kernel(double *edges, const double *map_w, const long long *map_counts,
+                              int ng, double alpha, double *scratch, int *status,
+                              double *damped_out) {
+  const int j = blockIdx.x;
+  double *d = scratch + (size_t)j * (5 * ng + 2);
+  double *sm = d + ng;
+  double *dw = sm + ng;
+  double *cum = dw + ng;        // ng+1
+  double *ne = cum + ng + 1;    // new interior edges [1, ng-1]
+  const double *w = map_w + (size_t)j * ng;
+  const long long *c = map_counts + (size_t)j * ng;
+  double *e = edges + (size_t)j * (ng + 1);
+  __shared__ double s_tot;
+  __shared__ int s_skip;
+  if (*status) return;
+  int nz = 0;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const double v = c[i] > 0 ? __ddiv_rn(w[i], (double)c[i]) : 0.0;
+    d[i] = v;
+    nz |= (v != 0.0);
+  }
+  nz = __syncthreads_or(nz);
+  if (!nz) {
+    if (damped_out)
+      for (int i = threadIdx.x; i < ng; i += blockDim.x) damped_out[(size_t)j * ng + i] = 0.0;
+    return;
+  }
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    double v;
+    if (i == 0) v = __dadd_rn(__dmul_rn(7.0, d[0]), d[1]);
+    else if (i == ng - 1) v = __dadd_rn(d[ng - 2], __dmul_rn(7.0, d[ng - 1]));
+    else v = __dadd_rn(__dadd_rn(d[i - 1], __dmul_rn(6.0, d[i])), d[i + 1]);
+    sm[i] = __ddiv_rn(v, 8.0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_tot = pw_sum_rt(sm, ng);
+    s_skip = !(s_tot > 0.0);
+  }
+  __syncthreads();
+  if (s_skip) {
+    if (damped_out)
+      for (int i = threadIdx.x; i < ng; i += blockDim.x) damped_out[(size_t)j * ng + i] = 0.0;
+    return;
+  }
+  const double tot = s_tot;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const double v = __ddiv_rn(sm[i], tot);
+    double r;
+    if (fabs(__dadd_rn(v, -1.0)) < 1e-15) r = 1.0;
+    else if (v >= 1e-30) r = np_scalar_pow(__ddiv_rn(__dadd_rn(v, -1.0), log(v)), alpha);
+    else r = 0.0;
+    dw[i] = r;
+    if (damped_out) damped_out[(size_t)j * ng + i] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_tot = pw_sum_rt(dw, ng);
+    s_skip = !(s_tot > 0.0);
+    if (!s_skip) {
+      cum[0] = 0.0;
+      for (int i = 0; i < ng; i++) cum[i + 1] = __dadd_rn(cum[i], dw[i]);
+    }
+  }
+  __syncthreads();
+  if (s_skip) return;
+  const double delta = __ddiv_rn(s_tot, (double)ng);
+  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) {
+    const double goal = __dmul_rn((double)i, delta);
+    // searchsorted(cum[1:], goal, 'left'): first iv with cum[iv+1] >= goal
+    int lo = 0, hi = ng - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cum[mid + 1] >= goal) hi = mid; else lo = mid + 1;
+    }
+    const int iv = lo;
+    const double frac = __ddiv_rn(__dadd_rn(goal, -cum[iv]), dw[iv]);
+    ne[i] = __dadd_rn(e[iv], __dmul_rn(frac, __dadd_rn(e[iv + 1], -e[iv])));
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+    const double a = i == 0 ? e[0] : ne[i];
+    const double b = i == ng - 1 ? e[ng] : ne[i + 1];
+    bad |= !(b > a);
+  }
+  bad = __syncthreads_or(bad);
+  if (bad) {
+    if (threadIdx.x == 0) atomicOr(status, 2);
+    return;
+  }
+  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) e[i] = ne[i];
+}
+
+// ---------------------------------------------------------- parity kernels --
+__global__ void philox_kernel(const uint64_t *block, const uint64_t *stream, const uint64_t *seed,
+                              long long n, uint64_t *out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const PhiloxKeys K(seed[i]);
+  uint64_t w0, w1;
+  philox((uint32_t)block[i], (uint32_t)(block[i] >> 32), (uint32_t)stream[i],
+         (uint32_t)(stream[i] >> 32), K, w0, w1);
+  out[2 * i] = w0;
+  out[2 * i + 1] = w1;
+}
+
+__global__ void uniform_kernel(const uint64_t *seed, const uint64_t *stream, const uint64_t *pos,
+                               long long n, double *out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const PhiloxKeys K(seed[i]);
+  uint64_t w0, w1;
+  const uint64_t blk = pos[i] >> 1;
+  philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)stream[i], (uint32_t)(stream[i] >> 32),
+         K, w0, w1);
+  out[i] = unit_from_word((pos[i] & 1) ? w1 : w0);
+}
+
+// kernels.sample_runs for runs [run_start, run_start+n): one thread per run,
+// cube by binary search (strat.run_to_cube, vp/strat.py:140-144).  The same
+// per-dimension arithmetic as the fill kernel.
+__global__ void sample_runs_kernel(unsigned long long seed, long long batch, long long run_base,
+                                   long long run_start, long long n, const long long *offsets,
+                                   long long n_cubes, const double *edges, int dims, int ng,
+                                   long long n_strat, double *x, double *jac, long long *idx,
+                                   long long *cube) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long r = run_start + i;
+  long long lo = 0, hi = n_cubes - 1;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (offsets[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  const long long c = lo;
+  cube[i] = c;
+  const PhiloxKeys K(seed);
+  const unsigned long long g = (unsigned long long)(run_base + r);
+  const unsigned long long sl = g % (unsigned long long)batch, k = g / (unsigned long long)batch;
+  const unsigned long long base = k * (unsigned long long)((dims + (dims & 1)) >> 1);
+  const double nsf = (double)n_strat, rns = 1.0 / nsf, ngf = (double)ng;
+  long long rem = c;
+  double jf = 1.0;
+  uint64_t w0 = 0, w1 = 0;
+  for (int j = 0; j < dims; j++) {
+    if ((j & 1) == 0) {
+      const unsigned long long blk = base + (unsigned long long)(j >> 1);
+      philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K, w0, w1);
+    }
+    const double u = unit_from_word((j & 1) ? w1 : w0);
+    const long long q = rem / n_strat, dig = rem - q * n_strat;
+    rem = q;
+    const double y = clamp_below_one(__dadd_rn(div_exact((double)dig, nsf, rns),
+                                               div_exact(u, nsf, rns)));
+    const double t = __dmul_rn(y, ngf);
+    const double sh = __dadd_rz(t, 4503599627370496.0);
+    int iv = __double2loint(sh);
+    double frac = __dadd_rn(t, -__dadd_rn(sh, -4503599627370496.0));
+    if (iv > ng - 1) { iv = ng - 1; frac = __dadd_rn(t, -(double)(ng - 1)); }
+    const double *e = edges + (size_t)j * (ng + 1) + iv;
+    const double dx = __dadd_rn(e[1], -e[0]);
+    x[i * dims + j] = __dadd_rn(e[0], __dmul_rn(frac, dx));
+    jf = __dmul_rn(jf, __dmul_rn(ngf, dx));
+    idx[i * dims + j] = iv;
+  }
+  jac[i] = jf;
+}
+
+}  // namespace vpb
