@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: integrand evaluations/s per VEGAS+ iteration on B200.
+
+Contract (BASELINE.json metric; one JSON line from rank 0):
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config cfg2|cfg1|cfg3|cfg4a|cfg4b|cfg5]
+
+* workload: BASELINE.json configs[1] = cfg2, the 8-D three-peak Gaussian
+  (multipeak8), n_eval = 1e8 per iteration per GPU (weak scaling: N GPUs
+  integrate n_eval = N * 1e8 with the same cube geometry, runs sharded by the
+  reference's partition rule and merged by one NCCL all-reduce), FP64,
+  n_intervals 1024, alpha 0.5, beta 0.75.  Synthetic: the integrand is a
+  closed-form function, nothing is loaded.
+* a step = one full iteration (plan -> fused fill -> [all-reduce] ->
+  results -> allocation -> refine) on device.  W warm-up iterations, then K
+  timed iterations; L2 is flushed (256 MiB write) before every timed
+  iteration, outside its CUDA-event window.
+* value = sum over ranks of evaluations (plan.total) / max-over-ranks device
+  time; e2e = the same metric through the public host-buffer call
+  (vpb_iteration_host: H2D of the map, D2H of estimate/variance/evals/map).
+* roofline: the fused fill kernel against the FP64 pipe (measured DFMA rate
+  on this GPU), algorithmic FP64 ops per evaluation from SURVEY.md §8(d)
+  with the transcendental costs of bench_costs below.
+* cpu_baseline: the C oracle port (oracle/) on this host's cores, rank 0,
+  N=1, bounded sample.  --impl reference: the same oracle as the reference
+  arm (the reference is Python and cannot travel to the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# --------------------------------------------------------------- workloads --
+# FP64 ops per evaluation (add/sub/mul/div = 1) and
+# transcendental calls per evaluation.  exp is costed at the FP64-pipe
+# instruction count of the device exp (devmath.cuh fast_exp: 2 clamps,
+# 4 reduction, 14 polynomial, 2 scaling = 22), cos at the libdevice cos
+# instruction count measured from SASS (~40).
+TRANSCENDENTAL_COST = {"exp": 22, "cos": 40}
+CONFIGS = {
+    "cfg1": dict(integrand="gaussian", dims=4, n_eval=10**6, ng=1000, flops=65, exp=1),
+    "cfg2": dict(integrand="multipeak8", dims=8, n_eval=10**8, ng=1024, flops=177, exp=3),
+    "cfg3": dict(integrand="ridge", dims=4, n_eval=10**8, ng=1024, flops=3227, exp=632),
+    "cfg4a": dict(integrand="genz_oscillatory6", dims=6, n_eval=10**9, ng=1024, flops=88, cos=1),
+    "cfg4b": dict(integrand="genz_productpeak6", dims=6, n_eval=10**9, ng=1024, flops=105),
+    "cfg5": dict(integrand="gaussian20", dims=20, n_eval=4 * 10**9, ng=1024, flops=305, exp=1),
+}
+METRIC = "integrand evals/sec per iteration (1/2/4/8 B200) + % FP64 roofline vs host CPU ref"
+UNIT = "evals/s"
+FIX_LAUNCHES_PER_ITER = 11   # our kernels per iteration (see capi.cu enqueue_iteration)
+
+
+def fp64_ops_per_eval(cfg) -> float:
+    return cfg["flops"] + sum(cfg.get(k, 0) * v for k, v in TRANSCENDENTAL_COST.items())
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled (every 50 ms) during the
+    timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.out = ""
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)   # first sample lands before the timed region
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+
+    def summary(self):
+        rows = [[c.strip() for c in l.split(",")] for l in self.out.strip().splitlines()
+                if l.strip()]
+        rows = [r for r in rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[5:9])
+                          if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# -------------------------------------------------------------- CPU oracle --
+def cpu_oracle_rate(cfg, n_eval_sample: int, iters: int = 2, workers: int | None = None):
+    """Time the oracle's fill on host cores: evals/s of the last iteration."""
+    import oracle as O
+    workers = workers or os.cpu_count() or 1
+    out = O.integrate(cfg["integrand"], [(0.0, 1.0)] * cfg["dims"], n_eval_sample,
+                      max_it=iters, n_intervals=cfg["ng"], workers=workers)
+    return out.evals[-1] / out.fill_seconds[-1], workers, out
+
+
+# ------------------------------------------------------------------ arms --
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")   # rendezvous + host-side max; NCCL lives in the .so
+    return world, rank, local
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args, cfgname, cfg, world, rank):
+    """--impl reference: the CPU oracle (port of the reference path) on all
+    host threads, same metric/config; rank 0 only."""
+    if rank != 0:
+        return
+    sample = int(os.environ.get("VPB_REF_SAMPLE", 10**7))
+    import oracle as O
+    workers = os.cpu_count() or 1
+    # one oracle "step" = one iteration of the same geometry at n_eval = sample
+    # (cube geometry identical: the 2^20 cube cap binds)
+    out = O.integrate(cfg["integrand"], [(0.0, 1.0)] * cfg["dims"], sample,
+                      max_it=args.warmup + args.steps, n_intervals=cfg["ng"], workers=workers)
+    ev = out.evals[args.warmup:]
+    secs = out.fill_seconds[args.warmup:]
+    value = sum(ev) / sum(secs)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfgname}: {cfg['integrand']} d={cfg['dims']} "
+                               f"ng={cfg['ng']}", "n_eval_per_iteration": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{args.warmup + args.steps} oracle iterations of "
+                                   f"{cfg['integrand']} at n_eval={sample} (same cube geometry "
+                                   f"as n_eval={cfg['n_eval']}); fill time only"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, cfgname, cfg, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_2408_09229_b200 as P
+    from paper_2408_09229_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n_eval = cfg["n_eval"] * world          # weak scaling: fixed work per GPU
+    steps, warmup = args.steps, args.warmup
+    conf = P.IntegratorConfig(n_eval=n_eval, max_it=warmup + steps + 1,
+                              n_intervals=cfg["ng"])
+    integ = P.Integrator(cfg["integrand"], [(0.0, 1.0)] * cfg["dims"], conf, device=local,
+                         distributed=(world > 1) or None, stream=stream.cuda_stream)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # measured FP64 peak (the roofline denominator; MEASURED_PEAKS.json has none)
+    peak = N.f64([0.0])
+    import ctypes
+    pk = ctypes.c_double()
+    N.check(N.load().vpb_fp64_peak(local, ctypes.byref(pk)))
+    peak_ops = pk.value
+
+    # ---- device-resident loop
+    integ.iterate(warmup)
+    integ.sync()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(steps):
+        flush.zero_()                         # L2 flush, outside the iteration's events
+        integ.iterate(1)
+    torch.cuda.synchronize(dev)
+    clocks.stop()
+    barrier(world)
+    est, var, evals = integ.history()
+    iter_ms, fill_ms = integ.timing_ms(warmup, steps)
+    t_max = allreduce_max(iter_ms, world)
+    evals_timed = int(np.sum(evals[warmup:warmup + steps]))   # plan.total is global
+    value = evals_timed / (t_max * 1e-3)
+    fill_ms_max = allreduce_max(fill_ms, world)
+
+    # ---- e2e through the host-buffer C call (a fresh context, same workload)
+    e_conf = P.IntegratorConfig(n_eval=n_eval, max_it=warmup + steps + 1,
+                                n_intervals=cfg["ng"])
+    e_integ = P.Integrator(cfg["integrand"], [(0.0, 1.0)] * cfg["dims"], e_conf, device=local,
+                           distributed=(world > 1) or None)
+    edges_host = N.f64(e_integ.edges())
+    pinned_in = torch.from_numpy(edges_host).pin_memory().numpy()
+    pinned_out = torch.empty(pinned_in.shape, dtype=torch.float64).pin_memory().numpy()
+    for _ in range(warmup):
+        e_integ.iteration_host(pinned_in, pinned_out)
+        pinned_in[...] = pinned_out
+    barrier(world)
+    t0 = time.perf_counter()
+    e_evals = 0
+    for _ in range(steps):
+        _, _, ev = e_integ.iteration_host(pinned_in, pinned_out)
+        pinned_in[...] = pinned_out
+        e_evals += ev
+    t1 = time.perf_counter()
+    e_time = allreduce_max(t1 - t0, world)
+    e2e_value = e_evals / e_time
+    h2d = pinned_in.nbytes
+    d2h = pinned_out.nbytes + 8 + 8 + 8
+    e_integ.close()
+
+    if rank == 0:
+        ops = fp64_ops_per_eval(cfg)
+        # fill kernel: per-rank evaluations = its shard of each plan
+        evals_per_rank = evals_timed / world
+        achieved = ops * evals_per_rank / (fill_ms_max * 1e-3)
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "fill_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(cfgname)
+            except Exception:
+                traffic = None
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            sample = int(os.environ.get("VPB_CPU_SAMPLE", cfg["n_eval"] // 10))
+            rate, cores, _ = cpu_oracle_rate(cfg, sample)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                   "sample": f"oracle (C port of vp/executor.parallel_fill, {cores} threads) "
+                             f"iteration 2 of {cfg['integrand']} at n_eval={sample} (same cube "
+                             f"geometry as n_eval={cfg['n_eval']}); fill time only"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": t_max / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (closed-form integrand, nothing loaded)",
+            "config": {"workload": f"{cfgname}: {cfg['integrand']} d={cfg['dims']}, "
+                                   f"n_eval={cfg['n_eval']:.0e}/iter/GPU, ng={cfg['ng']}",
+                       "n_eval_per_iteration": n_eval, "n_strat": integ.n_strat,
+                       "n_cubes": integ.n_cubes, "evals_per_step": evals_timed / steps,
+                       "parallelism": f"runs sharded over {world} GPU(s), NCCL all-reduce",
+                       "l2": "flushed (256 MiB write) before every timed iteration"},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
+                         "peak": peak_ops / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / peak_ops, "traffic": traffic,
+                         "kernel": "vpb::fill_kernel (fused Philox->map->integrand->histograms)",
+                         "convention": "FP64 pipe ops/s, add/mul/fma = 1 op; peak = measured "
+                                       "DFMA rate on this GPU (vpb_fp64_peak)",
+                         "ops_per_eval": ops, "fill_kernel_ms_per_step": fill_ms_max / steps,
+                         "fill_share_of_step": fill_ms_max / t_max},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": FIX_LAUNCHES_PER_ITER * steps,
+            "clocks": clocks.summary(),
+            "estimates": {"last": float(est[-1]), "sigma_last": float(np.sqrt(var[-1]))},
+        }
+        print(json.dumps(line), flush=True)
+    integ.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, args.config, cfg, world, rank)
+    else:
+        run_gpu(args, args.config, cfg, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

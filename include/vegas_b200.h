@@ -51,9 +51,9 @@ extern "C" {
 /* device integrand functors (registry names of vp/integrands.py:399-410 plus
  * the BASELINE-pinned synthetic integrands).  Parameter blobs: see
  * paper_2408_09229_b200/integrands.py. */
-#define VPB_GAUSSIAN 0          /* [mu, sigma, norm, 2 sigma^2]                  */
+#define VPB_GAUSSIAN 0          /* [mu, sigma, norm, 2 sigma^2, RN(1/(2 sigma^2))] */
 #define VPB_RIDGE 1             /* [n_centres, coef, window]                     */
-#define VPB_MULTIPEAK 2         /* [n_peaks, sigma, norm, 2 sigma^2, divisor, mu_k...] */
+#define VPB_MULTIPEAK 2         /* [n_peaks, sigma, norm, 2s^2, divisor, RN(1/2s^2), RN(1/divisor), mu_k...] */
 #define VPB_GENZ_OSCILLATORY 3  /* [2 pi u_1, a_0 .. a_{d-1}]                    */
 #define VPB_GENZ_PRODUCTPEAK 4  /* [a_0^-2 .. a_{d-1}^-2, u_0 .. u_{d-1}]        */
 #define VPB_SINEXP 5
@@ -134,6 +134,14 @@ int vpb_phase_times(vpb_ctx *ctx, double *map_ms, double *fill_ms, double *updat
 /* Device time (ms) of the last fill kernel and the number of fill launches. */
 int vpb_last_fill_ms(vpb_ctx *ctx, double *ms);
 int vpb_sync(vpb_ctx *ctx);
+/* Device time summed over iterations [first, first+count) of this reset:
+ * whole iterations and the fused fill kernel alone (CUDA events on the
+ * context's stream). */
+int vpb_timing(vpb_ctx *ctx, int32_t first, int32_t count, double *iter_ms,
+               double *fill_kernel_ms);
+/* Measured FP64 pipe throughput (DFMA chains on every SM; one FMA = 1 op):
+ * the roofline denominator for the FP64-issue-bound fill. */
+int vpb_fp64_peak(int32_t device, double *ops_per_s);
 
 /* State access (host buffers; synchronous). */
 int vpb_set_edges(vpb_ctx *ctx, const double *edges);

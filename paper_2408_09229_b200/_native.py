@@ -16,7 +16,7 @@ from .errors import (ContractViolationError, NativeLibraryError, NonFiniteIntegr
                      VegasError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libvegas_b200.so")
+LIB_PATH = os.environ.get("VPB_LIB_PATH") or os.path.join(HERE, "_lib", "libvegas_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "vegas_b200.h")
 
 VPB_OK = 0
@@ -72,6 +72,8 @@ SIGNATURES = {
     "vpb_phase_times": [_P, _c.POINTER(_F64), _c.POINTER(_F64), _c.POINTER(_F64)],
     "vpb_last_fill_ms": [_P, _c.POINTER(_F64)],
     "vpb_sync": [_P],
+    "vpb_timing": [_P, _I32, _I32, _c.POINTER(_F64), _c.POINTER(_F64)],
+    "vpb_fp64_peak": [_I32, _c.POINTER(_F64)],
     "vpb_set_edges": [_P, _P],
     "vpb_get_edges": [_P, _P],
     "vpb_set_allocation": [_P, _P],

@@ -20,6 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libvegas_b200.so")
+# tuning variants: VPB_BUILD_DEFINES="-DVPB_FILL_NT=640" VPB_BUILD_OUT=/path/lib.so
 ROOT = os.path.dirname(HERE)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -60,8 +61,12 @@ def _stale(objs) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    global LIB
+    extra = os.environ.get("VPB_BUILD_DEFINES", "").split()
+    if os.environ.get("VPB_BUILD_OUT"):
+        LIB = os.path.abspath(os.environ["VPB_BUILD_OUT"])
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(os.path.dirname(LIB), "obj" + ("_" + str(abs(hash(tuple(extra)))) if extra else ""))
     os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
@@ -72,7 +77,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(pair):
         src, obj = pair
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", inc, "-I", os.path.join(ROOT, "include"),
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", inc, "-I", os.path.join(ROOT, "include"),
                "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]

@@ -308,6 +308,13 @@ class Integrator:
                                           ctypes.byref(c)))
         return a.value, b.value, c.value
 
+    def timing_ms(self, first: int, count: int):
+        """(iteration ms, fill-kernel ms) summed over iterations [first, first+count)."""
+        a, k = ctypes.c_double(), ctypes.c_double()
+        N.check(self._lib.vpb_timing(self._ctx, int(first), int(count), ctypes.byref(a),
+                                     ctypes.byref(k)))
+        return a.value, k.value
+
     def last_fill_ms(self) -> float:
         t = ctypes.c_double()
         N.check(self._lib.vpb_last_fill_ms(self._ctx, ctypes.byref(t)))

@@ -196,7 +196,7 @@ struct vpb_ctx {
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   // timing
-  std::vector<std::array<cudaEvent_t, 4>> ev;
+  std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
   int it_enq = 0;   // iterations enqueued since reset
 };
@@ -216,6 +216,8 @@ FillArgs fill_args(vpb_ctx *c) {
   a.ngf = (double)c->ng;
   a.batch = c->batch;
   a.seed = c->seed;
+  a.keys = PhiloxKeys(c->seed);
+  a.nsdiv = MagicDiv((uint32_t)c->ns);
   const unsigned long long step = (unsigned long long)c->grid * FILL_TILE;
   a.dk = (long long)(step / (unsigned long long)c->batch);
   a.ds = (long long)(step % (unsigned long long)c->batch);
@@ -256,7 +258,7 @@ int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
   return VPB_OK;
 }
 
-int enqueue_fill(vpb_ctx *c, bool timed) {
+int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr) {
   const size_t m = (size_t)c->dims * c->ng;
   CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
   if (!c->smem_hist) {
@@ -265,7 +267,9 @@ int enqueue_fill(vpb_ctx *c, bool timed) {
   }
   FillArgs a = fill_args(c);
   if (timed) CK(cudaEventRecord(c->f0, c->st));
+  if (k0) CK(cudaEventRecord(k0, c->st));
   CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+  if (k1) CK(cudaEventRecord(k1, c->st));
   if (timed) CK(cudaEventRecord(c->f1, c->st));
   const long long nt = c->ntiles_cap;
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
@@ -320,10 +324,10 @@ int enqueue_iteration(vpb_ctx *c) {
   CK(cudaEventRecord(E[0], c->st));
   TRY(enqueue_plan(c, 1, nullptr));
   CK(cudaEventRecord(E[1], c->st));
-  TRY(enqueue_fill(c, true));
-  CK(cudaEventRecord(E[2], c->st));
+  TRY(enqueue_fill(c, true, E[2], E[3]));
+  CK(cudaEventRecord(E[4], c->st));
   TRY(enqueue_update(c, 1));
-  CK(cudaEventRecord(E[3], c->st));
+  CK(cudaEventRecord(E[5], c->st));
   mark_fail_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
   CK(cudaGetLastError());
   c->it_enq++;
@@ -659,12 +663,75 @@ int vpb_phase_times(vpb_ctx *c, double *map_ms, double *fill_ms, double *update_
   for (int i = 0; i < c->it_enq; i++) {
     float t;
     CK(cudaEventElapsedTime(&t, c->ev[i][0], c->ev[i][1])); a += t;
-    CK(cudaEventElapsedTime(&t, c->ev[i][1], c->ev[i][2])); b += t;
-    CK(cudaEventElapsedTime(&t, c->ev[i][2], c->ev[i][3])); u += t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][1], c->ev[i][4])); b += t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][4], c->ev[i][5])); u += t;
   }
   if (map_ms) *map_ms = a;
   if (fill_ms) *fill_ms = b;
   if (update_ms) *update_ms = u;
+  return VPB_OK;
+}
+
+int vpb_timing(vpb_ctx *c, int32_t first, int32_t count, double *iter_ms, double *fill_kernel_ms) {
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  if (first < 0 || count < 0 || first + count > c->it_enq)
+    return fail(VPB_ERR_INVALID, "iteration range outside the enqueued history");
+  double a = 0, k = 0;
+  for (int i = first; i < first + count; i++) {
+    float t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][0], c->ev[i][5])); a += t;
+    CK(cudaEventElapsedTime(&t, c->ev[i][2], c->ev[i][3])); k += t;
+  }
+  if (iter_ms) *iter_ms = a;
+  if (fill_kernel_ms) *fill_kernel_ms = k;
+  return VPB_OK;
+}
+
+namespace {
+__global__ void fp64_peak_kernel(double *out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4,
+         a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 1.0000001, cc = 1e-9;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      a0 = __fma_rn(a0, b, cc); a1 = __fma_rn(a1, b, cc); a2 = __fma_rn(a2, b, cc);
+      a3 = __fma_rn(a3, b, cc); a4 = __fma_rn(a4, b, cc); a5 = __fma_rn(a5, b, cc);
+      a6 = __fma_rn(a6, b, cc); a7 = __fma_rn(a7, b, cc);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace
+
+int vpb_fp64_peak(int32_t device, double *ops_per_s) {
+  if (device >= 0) CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0));
+  const int blocks = sms * 8, threads = 256, iters = 4000;
+  double *out = nullptr;
+  CK(cudaMalloc(&out, sizeof(double) * blocks * threads));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double best = 0.0;
+  fp64_peak_kernel<<<blocks, threads>>>(out, 100);
+  for (int r = 0; r < 4; r++) {
+    cudaEventRecord(e0);
+    fp64_peak_kernel<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = (double)blocks * threads * iters * 64.0;
+    best = std::max(best, ops / (ms * 1e-3));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  CK(cudaGetLastError());
+  *ops_per_s = best;
   return VPB_OK;
 }
 

@@ -18,6 +18,7 @@ namespace vpb {
 // the caller (they depend on the seed only -> uniform across the grid).
 struct PhiloxKeys {
   uint32_t k0[10], k1[10];
+  PhiloxKeys() = default;
   __host__ __device__ explicit PhiloxKeys(uint64_t seed) {
     uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
 #pragma unroll
@@ -75,34 +76,50 @@ __device__ __forceinline__ double div_exact(double a, double b, double r) {
 // NaN propagates (the non-finite detection of vp/executor.py:120-126 relies
 // on it).  The reference evaluates numpy's SIMD exp / libm exp, which are
 // not correctly rounded either: integrand values agree to a few ulp.
+// Coefficients live in constant memory so the DFMAs take c[][] operands
+// instead of materialising 64-bit immediates with UMOV pairs.
+static __constant__ double kExp[18] = {
+    6755399441055744.0,          // 0: 1.5 * 2^52 shifter
+    1.4426950408889634074,       // 1: 1/ln2
+    -6.93147180369123816490e-01, // 2: -ln2 hi (trailing zeros)
+    -1.90821492927058770002e-10, // 3: -ln2 lo
+    1.0 / 6227020800.0,          // 4: 1/13!
+    1.0 / 479001600.0,  1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+    1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0,   // 5..16
+    1400.0};                     // 17: clamp
 __device__ __forceinline__ double fast_exp(double x) {
-  x = (x < -1400.0) ? -1400.0 : x;
-  x = (x > 1400.0) ? 1400.0 : x;
-  const double SH = 6755399441055744.0;   // 1.5 * 2^52
-  double kd = __fma_rn(x, 1.4426950408889634074, SH);
+  x = (x < -kExp[17]) ? -kExp[17] : x;
+  x = (x > kExp[17]) ? kExp[17] : x;
+  double kd = __fma_rn(x, kExp[1], kExp[0]);
   const int k = __double2loint(kd);
-  kd = __dadd_rn(kd, -SH);
-  double r = __fma_rn(kd, -6.93147180369123816490e-01, x);   // ln2 hi (trailing zeros)
-  r = __fma_rn(kd, -1.90821492927058770002e-10, r);            // ln2 lo
-  double p = 1.0 / 6227020800.0;            // 1/13!
-  p = __fma_rn(p, r, 1.0 / 479001600.0);    // 1/12!
-  p = __fma_rn(p, r, 1.0 / 39916800.0);
-  p = __fma_rn(p, r, 1.0 / 3628800.0);
-  p = __fma_rn(p, r, 1.0 / 362880.0);
-  p = __fma_rn(p, r, 1.0 / 40320.0);
-  p = __fma_rn(p, r, 1.0 / 5040.0);
-  p = __fma_rn(p, r, 1.0 / 720.0);
-  p = __fma_rn(p, r, 1.0 / 120.0);
-  p = __fma_rn(p, r, 1.0 / 24.0);
-  p = __fma_rn(p, r, 1.0 / 6.0);
-  p = __fma_rn(p, r, 0.5);
-  p = __fma_rn(p, r, 1.0);
-  p = __fma_rn(p, r, 1.0);
+  kd = __dadd_rn(kd, -kExp[0]);
+  double r = __fma_rn(kd, kExp[2], x);
+  r = __fma_rn(kd, kExp[3], r);
+  double p = kExp[4];
+#pragma unroll
+  for (int i = 5; i <= 16; i++) p = __fma_rn(p, r, kExp[i]);
+  p = __fma_rn(p, r, kExp[16]);
   const int k1 = k >> 1, k2 = k - k1;
   const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
   const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
   return __dmul_rn(__dmul_rn(p, s1), s2);
 }
+
+// 32-bit unsigned division by a runtime-constant divisor D in [1, 2^31]
+// for numerators n < 2^31: q = (umulhi(n, m) + n) >> l with l = ceil(log2 D),
+// m = floor(2^32 (2^l - D) / D) + 1 (Granlund-Montgomery).  Used for the
+// mixed-radix cube digits (vp/kernels.py:76-77); checked exhaustively in
+// tests/test_capi_cpu.py::test_magic_division.
+struct MagicDiv {
+  uint32_t m, l, d;
+  MagicDiv() = default;
+  __host__ __device__ explicit MagicDiv(uint32_t D) : d(D) {
+    l = 0;
+    while (l < 32 && (1ull << l) < D) l++;
+    m = (uint32_t)((((1ull << 32) * ((1ull << l) - D)) / D) + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> l; }
+};
 
 // ----------------------------------------------- numpy pairwise summation --
 // numpy float64 add.reduce of a contiguous row: used for

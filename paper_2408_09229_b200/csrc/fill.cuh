@@ -31,8 +31,14 @@
 
 namespace vpb {
 
-constexpr int FILL_NT = 512;   // threads per CTA
-constexpr int FILL_RPT = 4;    // consecutive runs per thread per tile
+#ifndef VPB_FILL_NT
+#define VPB_FILL_NT 768
+#endif
+#ifndef VPB_FILL_RPT
+#define VPB_FILL_RPT 16
+#endif
+constexpr int FILL_NT = VPB_FILL_NT;    // threads per CTA (one CTA per SM)
+constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per thread per tile
 constexpr int FILL_TILE = FILL_NT * FILL_RPT;
 constexpr int FILL_WMAX = FILL_TILE / 2 + 4;   // cube offsets window per tile
 constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
@@ -57,6 +63,8 @@ struct FillArgs {
   double nsf, rns, ngf;         // N, RN(1/N), ng as doubles
   long long batch;
   unsigned long long seed;
+  PhiloxKeys keys;              // round keys (host-computed; constant bank operands)
+  MagicDiv nsdiv;               // division by n_strat (cube digits)
   long long dk, ds;             // per-grid-stride advance of (k, slot)
   const Sched *sched;
   const int *tile_cube;         // [ntiles+1]
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     for (int i = tid; i < a.n_strat; i += FILL_NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
 
   const Sched S = *a.sched;
-  const PhiloxKeys K(a.seed);
+  const PhiloxKeys &K = a.keys;
   const long long lo = S.lo, hi = S.hi, ntiles = S.ntiles;
   const unsigned long long batch = (unsigned long long)a.batch;
   const unsigned long long stride_half = (unsigned long long)((d + (d & 1)) >> 1);
@@ -187,11 +195,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       unsigned long long k = kk, sl = slot;
       double dq[MAXD];
       auto load_digits = [&](long long c) {
-        long long rem = c;
+        uint32_t rem = (uint32_t)c;   // n_cubes < 2^31
 #pragma unroll
         for (int j = 0; j < (D > 0 ? D : d); j++) {
-          const long long q = rem / a.n_strat;
-          const long long dig = rem - q * a.n_strat;
+          const uint32_t q = a.nsdiv.div(rem);
+          const uint32_t dig = rem - q * a.nsdiv.d;
           rem = q;
           dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
         }
@@ -235,16 +243,18 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
                    w0, w1);
           }
           const double u = unit_from_word((j & 1) ? w1 : w0);
-          const double y = clamp_below_one(__dadd_rn(dq[j], div_exact(u, a.nsf, a.rns)));
+          // y >= 1 -> nextafter(1, 0): fmin is exactly that clamp (y is never NaN)
+          const double y = fmin(__dadd_rn(dq[j], div_exact(u, a.nsf, a.rns)),
+                                0.99999999999999988898);
           const double t = __dmul_rn(y, a.ngf);
           // trunc(t) for 0 <= t < 2^31 via the 2^52 shifter in round-toward-zero
           const double sh = __dadd_rz(t, 4503599627370496.0);
           int ivj = __double2loint(sh);
           double frac = __dadd_rn(t, -__dadd_rn(sh, -4503599627370496.0));
-          if (ivj > ng - 1) {   // t rounded up to ng (y = 1 - 2^-53)
-            ivj = ng - 1;
-            frac = __dadd_rn(t, -(double)(ng - 1));
-          }
+          // t rounded up to ng (y = 1 - 2^-53): iv = ng-1, frac = t - (ng-1) = 1
+          const bool over = ivj >= ng;
+          ivj = over ? ng - 1 : ivj;
+          frac = over ? 1.0 : frac;
           const double *e = s_edges + j * (ng + 1) + ivj;
           const double elo = e[0];
           const double dx = __dadd_rn(e[1], -elo);
@@ -264,10 +274,35 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           v2 = __dadd_rn(v2, w2);
           // ---- interval histograms (vp/kernels.py:100-105)
           if (a.smem_hist) {
+            // Lane-rotated dimension order: at step s lane l updates dim
+            // (s + l) mod d.  Lanes of a warp usually sit in the same cube,
+            // i.e. the same stratum of every axis, so with a common order
+            // most CAS instructions have two lanes on one interval and
+            // retry; rotated, a step's lanes are spread over d histograms.
+            const int rot = lane % d;
+            int ivr[MAXD];
+#pragma unroll
+            for (int j = 0; j < (D > 0 ? D : d); j++) ivr[j] = iv[j];
+            if constexpr (D > 1) {
+#pragma unroll
+              for (int b = 1; b < D; b <<= 1) {   // barrel rotation by rot
+                const bool on = (rot & b) != 0;
+                int t[D];
+#pragma unroll
+                for (int j = 0; j < D; j++) t[j] = on ? ivr[(j + b) % D] : ivr[j];
+#pragma unroll
+                for (int j = 0; j < D; j++) ivr[j] = t[j];
+              }
+            } else if constexpr (D == 0) {
+              for (int j = 0; j < d; j++) ivr[j] = iv[(j + rot) % d];
+            }
+            int jj = rot;
 #pragma unroll
             for (int j = 0; j < (D > 0 ? D : d); j++) {
-              atomicAdd(&s_hw[j * ng + iv[j]], w2);
-              atomicAdd(&s_hc[j * ng + iv[j]], 1u);
+              const int idx = jj * ng + ivr[j];
+              atomicAdd(&s_hw[idx], w2);
+              atomicAdd(&s_hc[idx], 1u);
+              jj = (jj + 1 == d) ? 0 : jj + 1;
             }
           } else {
 #pragma unroll

@@ -43,22 +43,25 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
       t[j] = __dmul_rn(u, u);
     }
     const double r2 = row_sum<D>(t, d);
-    return __dmul_rn(P.p[2], fast_exp(-__ddiv_rn(r2, P.p[3])));
+    // -r2 / (2 sigma^2): Markstein with the host's RN(1/(2 sigma^2)) (bitwise
+    // IEEE division for these divisors, tools/proofs/markstein_general.c)
+    return __dmul_rn(P.p[2], fast_exp(-div_exact(r2, P.p[3], P.p[4])));
   } else if constexpr (ID == VPB_MULTIPEAK) {
     // (1/3) sum_k norm * exp(-|x - mu_k|^2 / (2 sigma^2))
+    // p = [n_peaks, sigma, norm, 2 sigma^2, divisor, RN(1/2sigma^2), RN(1/divisor), mu_k...]
     const int np = (int)P.p[0];
     double out = 0.0;
     for (int k = 0; k < np; k++) {
       double t[MAXD];
 #pragma unroll
       for (int j = 0; j < (D > 0 ? D : d); j++) {
-        const double u = __dadd_rn(x[j], -P.p[5 + k]);
+        const double u = __dadd_rn(x[j], -P.p[7 + k]);
         t[j] = __dmul_rn(u, u);
       }
       const double r2 = row_sum<D>(t, d);
-      out = __dadd_rn(out, __dmul_rn(P.p[2], fast_exp(-__ddiv_rn(r2, P.p[3]))));
+      out = __dadd_rn(out, __dmul_rn(P.p[2], fast_exp(-div_exact(r2, P.p[3], P.p[5]))));
     }
-    return __ddiv_rn(out, P.p[4]);
+    return div_exact(out, P.p[4], P.p[6]);
   } else if constexpr (ID == VPB_RIDGE) {
     // windowed sum over the 1000 diagonal centres        vp/integrands.py:154-182
     double xs[MAXD];

@@ -120,7 +120,8 @@ GAUSSIAN_SIGMA = 0.01
 def _gauss_params(mu, sigma):
     def fn(d):
         norm = (2.0 * math.pi * sigma ** 2) ** (-d / 2.0)
-        return [mu, sigma, norm, 2.0 * sigma ** 2]
+        denom = 2.0 * sigma ** 2
+        return [mu, sigma, norm, denom, 1.0 / denom]
     return fn
 
 
@@ -143,7 +144,8 @@ MP_MUS = (0.25, 0.5, 0.75)
 
 def _mp_params(d):
     norm = (2.0 * math.pi * MP_SIGMA ** 2) ** (-d / 2.0)
-    return [float(len(MP_MUS)), MP_SIGMA, norm, 2.0 * MP_SIGMA ** 2, float(len(MP_MUS))] + \
+    denom, div = 2.0 * MP_SIGMA ** 2, float(len(MP_MUS))
+    return [float(len(MP_MUS)), MP_SIGMA, norm, denom, div, 1.0 / denom, 1.0 / div] + \
         list(MP_MUS)
 
 
