@@ -15,6 +15,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -199,6 +200,14 @@ struct vpb_ctx {
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
   int it_enq = 0;   // iterations enqueued since reset
+  // one iteration captured as a CUDA graph (launched once per iteration;
+  // the six phase-event nodes are re-pointed at the iteration's events)
+  bool use_graph = true;
+  cudaStream_t cap_st = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::array<cudaGraphNode_t, 6> ev_nodes{};
+  bool capturing = false;
 };
 
 namespace {
@@ -241,6 +250,12 @@ FillArgs fill_args(vpb_ctx *c) {
   return a;
 }
 
+// event records become graph nodes only when flagged external during capture
+cudaError_t rec_event(vpb_ctx *c, cudaEvent_t e) {
+  return c->capturing ? cudaEventRecordWithFlags(e, c->st, cudaEventRecordExternal)
+                      : cudaEventRecord(e, c->st);
+}
+
 int setdev(vpb_ctx *c) {
   CK(cudaSetDevice(c->dev));
   return VPB_OK;
@@ -253,7 +268,8 @@ int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
                                              c->h_evals, record, c->ntiles_cap, c->status,
                                              explicit_rb);
   plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,
-                                                             c->offsets, c->sched, c->tile_cube);
+                                                             c->offsets, c->sched, c->tile_cube,
+                                                             c->status);
   CK(cudaGetLastError());
   return VPB_OK;
 }
@@ -267,14 +283,14 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   }
   FillArgs a = fill_args(c);
   if (timed) CK(cudaEventRecord(c->f0, c->st));
-  if (k0) CK(cudaEventRecord(k0, c->st));
+  if (k0) CK(rec_event(c, k0));
   CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
-  if (k1) CK(cudaEventRecord(k1, c->st));
+  if (k1) CK(rec_event(c, k1));
   if (timed) CK(cudaEventRecord(c->f1, c->st));
   const long long nt = c->ntiles_cap;
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
   if (c->smem_hist) {
-    hist_reduce_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->st>>>(
+    hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
         c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
   } else {
     CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, c->st));
@@ -296,14 +312,14 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
 int enqueue_update(vpb_ctx *c, int record) {
   const double V = 1.0 / (double)c->n_cubes;
   const PwPlanDev pd = c->pw.dev();
-  results_leaf_kernel<<<(unsigned)((pd.L + 127) / 128), 128, 0, c->st>>>(
+  results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
       c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, pd, c->d_h, c->dp, c->pwvals, c->status);
   results_tree_kernel<<<1, 1024, 0, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
                                              c->h_var, c->sched, c->status, record);
   alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, c->beta,
                                                        (double)c->n_eval, c->uniform_nh, c->sc, 0,
                                                        c->n_h, c->bsum, c->status);
-  refine_kernel<<<c->dims, 256, 0, c->st>>>(c->edges, c->map_w, c->map_counts, c->ng, c->alpha,
+  refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->st>>>(c->edges, c->map_w, c->map_counts, c->ng, c->alpha,
                                             c->refine_scr, c->status, nullptr);
   CK(cudaGetLastError());
   return VPB_OK;
@@ -312,24 +328,71 @@ int enqueue_update(vpb_ctx *c, int record) {
 __global__ void mark_fail_kernel(const int *status, int *fail_it, const Sched *sched) {
   if (*status && *fail_it < 0) *fail_it = sched->it;
 }
-__global__ void guarded_set_it_kernel(Sched *sched, int it, const int *status) {
-  if (!*status) sched->it = it;
+// iteration index lives on device (so one captured graph serves every
+// iteration); frozen once an iteration failed
+__global__ void step_it_kernel(Sched *sched, const int *status) {
+  if (!*status) sched->it = sched->it + 1;
+}
+
+int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
+  step_it_kernel<<<1, 1, 0, c->st>>>(c->sched, c->status);
+  CK(rec_event(c, E[0]));
+  TRY(enqueue_plan(c, 1, nullptr));
+  CK(rec_event(c, E[1]));
+  TRY(enqueue_fill(c, false, E[2], E[3]));
+  CK(rec_event(c, E[4]));
+  TRY(enqueue_update(c, 1));
+  CK(rec_event(c, E[5]));
+  mark_fail_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
+  CK(cudaGetLastError());
+  return VPB_OK;
+}
+
+int build_graph(vpb_ctx *c) {
+  if (!c->cap_st) CK(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+  cudaStream_t run_st = c->st;
+  c->st = c->cap_st;
+  CK(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeRelaxed));
+  c->capturing = true;
+  int rc = enqueue_iteration_body(c, c->ev[0]);
+  c->capturing = false;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->cap_st, &g);
+  c->st = run_st;
+  if (rc != VPB_OK) { if (g) cudaGraphDestroy(g); return rc; }
+  CK(e);
+  c->graph = g;
+  CK(cudaGraphInstantiate(&c->gexec, g, 0));
+  size_t n = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(g, nodes.data(), &n));
+  int found = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t));
+    if (t != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+    for (int k = 0; k < 6; k++)
+      if (ev == c->ev[0][k]) { c->ev_nodes[k] = nd; found++; }
+  }
+  if (found != 6) return fail(VPB_ERR_CUDA, "graph capture lost the phase events");
+  return VPB_OK;
 }
 
 int enqueue_iteration(vpb_ctx *c) {
   if (c->it_enq >= c->max_it)
     return fail(VPB_ERR_INVALID, "iteration history capacity (max_it) exhausted");
   auto &E = c->ev[c->it_enq];
-  guarded_set_it_kernel<<<1, 1, 0, c->st>>>(c->sched, c->it_enq, c->status);
-  CK(cudaEventRecord(E[0], c->st));
-  TRY(enqueue_plan(c, 1, nullptr));
-  CK(cudaEventRecord(E[1], c->st));
-  TRY(enqueue_fill(c, true, E[2], E[3]));
-  CK(cudaEventRecord(E[4], c->st));
-  TRY(enqueue_update(c, 1));
-  CK(cudaEventRecord(E[5], c->st));
-  mark_fail_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
-  CK(cudaGetLastError());
+  if (c->use_graph) {
+    if (!c->gexec) TRY(build_graph(c));
+    for (int k = 0; k < 6; k++)
+      CK(cudaGraphExecEventRecordNodeSetEvent(c->gexec, c->ev_nodes[k], E[k]));
+    CK(cudaGraphLaunch(c->gexec, c->st));
+  } else {
+    TRY(enqueue_iteration_body(c, E));
+  }
   c->it_enq++;
   return VPB_OK;
 }
@@ -379,6 +442,9 @@ void free_ctx(vpb_ctx *c) {
       if (e) cudaEventDestroy(e);
   if (c->f0) cudaEventDestroy(c->f0);
   if (c->f1) cudaEventDestroy(c->f1);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
@@ -437,6 +503,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   c->beta = d->beta;
   c->id = d->integrand;
   c->max_it = d->max_it;
+  if (const char *g = std::getenv("VPB_NO_GRAPH")) c->use_graph = !(g[0] == '1');
   c->P.n = d->n_params;
   for (int i = 0; i < d->n_params; i++) c->P.p[i] = d->params[i];
   c->bounds.assign(d->bounds, d->bounds + 2 * d->dims);
@@ -494,7 +561,11 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   A(c->status, 1);
   A(c->fail_it, 1);
   A(c->err_run, 1);
-  A(c->refine_scr, (size_t)c->dims * (5 * c->ng + 2));
+  A(c->refine_scr, (size_t)c->dims * (6 * c->ng + 3));
+  if (refine_smem_bytes(c->ng) > 48 * 1024 &&
+      cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)refine_smem_bytes(c->ng)) != cudaSuccess)
+    return bail(fail(VPB_ERR_CUDA, "refine smem attribute"));
   A(c->explicit_rb, 1);
   // fill geometry: shared histograms when they fit next to the edges
   int sms = 148;
@@ -554,11 +625,16 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
   TRY(setdev(c));
   ncclUniqueId uid;
   std::memcpy(&uid, id, 128);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->comm) ncclCommDestroy(c->comm);
   c->comm = nullptr;
   NK(ncclCommInitRank(&c->comm, world, uid, rank));
   c->world = world;
   c->rank = rank;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   return VPB_OK;
 }
 
@@ -566,6 +642,8 @@ int vpb_set_shard(vpb_ctx *c, int32_t world, int32_t rank) {
   if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
   c->world = world;
   c->rank = rank;
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   return VPB_OK;
 }
 
@@ -574,6 +652,7 @@ int vpb_reset(vpb_ctx *c) {
   CK(cudaStreamSynchronize(c->st));
   TRY(upload_uniform_edges(c));
   Sched s{};
+  s.it = -1;   // step_it_kernel pre-increments
   CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
   Scalars z{};
   CK(cudaMemcpy(c->sc, &z, sizeof(z), cudaMemcpyHostToDevice));
@@ -739,7 +818,8 @@ int vpb_last_fill_ms(vpb_ctx *c, double *ms) {
   TRY(setdev(c));
   CK(cudaStreamSynchronize(c->st));
   float t = 0;
-  CK(cudaEventElapsedTime(&t, c->f0, c->f1));
+  if (c->it_enq > 0) CK(cudaEventElapsedTime(&t, c->ev[c->it_enq - 1][2], c->ev[c->it_enq - 1][3]));
+  else CK(cudaEventElapsedTime(&t, c->f0, c->f1));
   *ms = t;
   return VPB_OK;
 }
@@ -1010,7 +1090,8 @@ int vpb_fill_host(const int64_t *offsets, int64_t n_cubes, const double *edges, 
   CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
   // rebuild the tile table for the explicit range (block prefixes still in bsum)
   plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,
-                                                             c->offsets, c->sched, c->tile_cube);
+                                                             c->offsets, c->sched, c->tile_cube,
+                                                             c->status);
   CK(cudaGetLastError());
   TRY(enqueue_fill(c, false));
   CK(cudaStreamSynchronize(c->st));
@@ -1102,7 +1183,7 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   CK(cudaMemset(st.p, 0, sizeof(int)));
   CK(cudaMemset(sch.p, 0, sizeof(Sched)));
   const double V = 1.0 / (double)n;
-  results_leaf_kernel<<<nblk(pw.L, 128), 128>>>(a.p, b.p, doff.p, n, V, beta, pw.dev(), dh.p,
+  results_leaf_kernel<<<nblk(8LL * pw.L, 256), 256>>>(a.p, b.p, doff.p, n, V, beta, pw.dev(), dh.p,
                                                 dp.p, vals.p, st.p);
   results_tree_kernel<<<1, 1024>>>(pw.dev(), vals.p, n, V, sc.p, he.p, hv.p, sch.p, st.p, 0);
   CK(cudaGetLastError());
@@ -1176,7 +1257,7 @@ int vpb_build_plan_host(const int64_t *n_h, int64_t n, int64_t *offsets) {
   CK(cudaMemset(rb.p, 0, sizeof(long long)));
   nh_blocksum_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p);
   plan_scan_kernel<<<1, PLAN_NT>>>(bs.p, nb, sch.p, 1, 0, ev.p, 0, tot / FILL_TILE + 2, st.p, rb.p);
-  plan_offsets_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p, off.p, sch.p, tc.p);
+  plan_offsets_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p, off.p, sch.p, tc.p, st.p);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return off.down((long long *)offsets, n + 1);
@@ -1190,7 +1271,10 @@ int vpb_smooth_and_damp_host(const double *map_w, const int64_t *map_counts, int
   DBuf<long long> cnt;
   DBuf<int> st;
   TRY(w.up(map_w, m)); TRY(cnt.up((const long long *)map_counts, m));
-  TRY(e.alloc((size_t)dims * (ng + 1))); TRY(scr.alloc((size_t)dims * (5 * ng + 2)));
+  TRY(e.alloc((size_t)dims * (ng + 1))); TRY(scr.alloc((size_t)dims * (6 * ng + 3)));
+  if (refine_smem_bytes(ng) > 48 * 1024)
+    CK(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)refine_smem_bytes(ng)));
   TRY(o.alloc(m)); TRY(st.alloc(1));
   // uniform dummy edges; only the damped weights are returned
   std::vector<double> he((size_t)dims * (ng + 1));
@@ -1198,7 +1282,7 @@ int vpb_smooth_and_damp_host(const double *map_w, const int64_t *map_counts, int
     for (int i = 0; i <= ng; i++) he[(size_t)j * (ng + 1) + i] = (double)i / ng;
   CK(cudaMemcpy(e.p, he.data(), sizeof(double) * he.size(), cudaMemcpyHostToDevice));
   CK(cudaMemset(st.p, 0, sizeof(int)));
-  refine_kernel<<<dims, 256>>>(e.p, w.p, cnt.p, ng, alpha, scr.p, st.p, o.p);
+  refine_kernel<<<dims, REFINE_NT, refine_smem_bytes(ng)>>>(e.p, w.p, cnt.p, ng, alpha, scr.p, st.p, o.p);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return o.down(out, m);

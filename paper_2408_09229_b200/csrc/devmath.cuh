@@ -54,7 +54,8 @@ __device__ __forceinline__ void philox(uint32_t c0, uint32_t c1, uint32_t c2, ui
 __device__ __forceinline__ double unit_from_word(uint64_t w) {
   const uint64_t m = w >> 11;
   const double t = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
-  const double half = (m >> 52) ? 0.5 : 0.0;
+  // bit 52 of m (= bit 63 of w) adds 0.5: build 0.5 / 0.0 from the high word only
+  const double half = __hiloint2double((int)(w >> 63) * 0x3FE00000, 0);
   return __fma_rn(__dadd_rn(t, -1.0), 0.5, half);   // both steps exact
 }
 
@@ -87,9 +88,7 @@ static __constant__ double kExp[18] = {
     1.0 / 479001600.0,  1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
     1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0,   // 5..16
     1400.0};                     // 17: clamp
-__device__ __forceinline__ double fast_exp(double x) {
-  x = (x < -kExp[17]) ? -kExp[17] : x;
-  x = (x > kExp[17]) ? kExp[17] : x;
+__device__ __forceinline__ double fast_exp_core(double x) {
   double kd = __fma_rn(x, kExp[1], kExp[0]);
   const int k = __double2loint(kd);
   kd = __dadd_rn(kd, -kExp[0]);
@@ -103,6 +102,19 @@ __device__ __forceinline__ double fast_exp(double x) {
   const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
   const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
   return __dmul_rn(__dmul_rn(p, s1), s2);
+}
+
+// General exp: NaN-propagating clamps (non-finite integrand detection).
+__device__ __forceinline__ double fast_exp(double x) {
+  x = (x < -kExp[17]) ? -kExp[17] : x;
+  x = (x > kExp[17]) ? kExp[17] : x;
+  return fast_exp_core(x);
+}
+
+// exp of a finite, non-positive argument (Gaussian exponents of finite
+// points): one DMNMX clamp.
+__device__ __forceinline__ double fast_exp_nonpos(double x) {
+  return fast_exp_core(fmax(x, -kExp[17]));
 }
 
 // 32-bit unsigned division by a runtime-constant divisor D in [1, 2^31]

@@ -32,7 +32,7 @@
 namespace vpb {
 
 #ifndef VPB_FILL_NT
-#define VPB_FILL_NT 768
+#define VPB_FILL_NT 640
 #endif
 #ifndef VPB_FILL_RPT
 #define VPB_FILL_RPT 16
@@ -104,6 +104,7 @@ __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
   b += (size_t)FILL_NT * (2 * sizeof(double) + sizeof(int));           // scan scratch
   b += 32 * (2 * sizeof(double) + sizeof(int));                        // warp aggregates
+  b += 16;                                                              // block flags
   return b;
 }
 
@@ -143,6 +144,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   double *s_w2 = reinterpret_cast<double *>(smem_raw + off);
   off += 32 * sizeof(double);
   int *s_wf = reinterpret_cast<int *>(smem_raw + off);
+  off += 32 * sizeof(int);
+  int *s_flag = reinterpret_cast<int *>(smem_raw + off);
 
   for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
   if (a.smem_hist)
@@ -150,12 +153,14 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   if (dq_tab)
     for (int i = tid; i < a.n_strat; i += FILL_NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
 
+  if (tid == 0) s_flag[0] = *a.status;   // an earlier iteration failed: nothing to fill
   const Sched S = *a.sched;
   const PhiloxKeys &K = a.keys;
   const long long lo = S.lo, hi = S.hi, ntiles = S.ntiles;
   const unsigned long long batch = (unsigned long long)a.batch;
   const unsigned long long stride_half = (unsigned long long)((d + (d & 1)) >> 1);
   __syncthreads();
+  if (s_flag[0]) return;   // block-uniform
 
   // (k, slot) of this thread's first run in its first tile; advanced per grid stride
   unsigned long long g0 = (unsigned long long)(S.run_base + lo + (long long)blockIdx.x * FILL_TILE +
@@ -249,12 +254,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           const double t = __dmul_rn(y, a.ngf);
           // trunc(t) for 0 <= t < 2^31 via the 2^52 shifter in round-toward-zero
           const double sh = __dadd_rz(t, 4503599627370496.0);
-          int ivj = __double2loint(sh);
-          double frac = __dadd_rn(t, -__dadd_rn(sh, -4503599627370496.0));
-          // t rounded up to ng (y = 1 - 2^-53): iv = ng-1, frac = t - (ng-1) = 1
-          const bool over = ivj >= ng;
-          ivj = over ? ng - 1 : ivj;
-          frac = over ? 1.0 : frac;
+          // iv = min(trunc t, ng-1) and frac = t - iv, branch-free: when t
+          // rounds up to ng (y within ulps of 1) this gives iv = ng-1, frac = 1
+          const int ivj = min(__double2loint(sh), ng - 1);
+          const double frac =
+              __dadd_rn(t, -fmin(__dadd_rn(sh, -4503599627370496.0), a.ngf - 1.0));
           const double *e = s_edges + j * (ng + 1) + ivj;
           const double elo = e[0];
           const double dx = __dadd_rn(e[1], -elo);

@@ -45,7 +45,7 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     const double r2 = row_sum<D>(t, d);
     // -r2 / (2 sigma^2): Markstein with the host's RN(1/(2 sigma^2)) (bitwise
     // IEEE division for these divisors, tools/proofs/markstein_general.c)
-    return __dmul_rn(P.p[2], fast_exp(-div_exact(r2, P.p[3], P.p[4])));
+    return __dmul_rn(P.p[2], fast_exp_nonpos(-div_exact(r2, P.p[3], P.p[4])));
   } else if constexpr (ID == VPB_MULTIPEAK) {
     // (1/3) sum_k norm * exp(-|x - mu_k|^2 / (2 sigma^2))
     // p = [n_peaks, sigma, norm, 2 sigma^2, divisor, RN(1/2sigma^2), RN(1/divisor), mu_k...]
@@ -59,7 +59,7 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
         t[j] = __dmul_rn(u, u);
       }
       const double r2 = row_sum<D>(t, d);
-      out = __dadd_rn(out, __dmul_rn(P.p[2], fast_exp(-div_exact(r2, P.p[3], P.p[5]))));
+      out = __dadd_rn(out, __dmul_rn(P.p[2], fast_exp_nonpos(-div_exact(r2, P.p[3], P.p[5]))));
     }
     return div_exact(out, P.p[4], P.p[6]);
   } else if constexpr (ID == VPB_RIDGE) {
@@ -100,8 +100,9 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     double acc = 0.0;
     for (int i = lo; i <= hi; i++) {
       const double dc = __dadd_rn(div_exact((double)i, spacing, rsp), -mu);
-      acc = __dadd_rn(acc, fast_exp(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
+      acc = __dadd_rn(acc, fast_exp_nonpos(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
     }
+    // q0 = s2 - s1^2/4 >= 0 up to rounding: the general exp
     return __dmul_rn(__dmul_rn(P.p[1], fast_exp(__dmul_rn(-100.0, q0))), acc);
   } else if constexpr (ID == VPB_GENZ_OSCILLATORY) {
     // cos(2 pi u_1 + a . x)

@@ -37,65 +37,68 @@ __device__ __forceinline__ double np_scalar_pow(double x, double e) {
 }
 
 // ---------------------------------------------------------------- results --
-// One thread per pairwise leaf over the cubes.  Per cube (vp/strat.py:199-207):
-//   c = n_h (every planned run was evaluated once), m = s1/c,
-//   rv = max(s2/c - m*m, 0), d_h = sqrt(rv)*V, and for the allocation
-//   dp = d_h**beta.  Leaf partial sums of m, rv/c and dp follow numpy's
-//   8-accumulator leaf exactly.
+// Per cube (vp/strat.py:199-207): c = n_h (every planned run was evaluated
+// once), m = s1/c, rv = max(s2/c - m*m, 0), d_h = sqrt(rv)*V, and for the
+// allocation dp = d_h**beta.  Leaf partial sums of m, rv/c and dp follow
+// numpy's 8-accumulator leaf exactly: 8 lanes per leaf, lane j owns
+// accumulator r[j] (elements j, j+8, ...), the lanes combine as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) (IEEE addition is commutative, so the
+// butterfly gives numpy's bits), and lane 0 adds the tail sequentially.
+__device__ __forceinline__ void cube_terms(const double *s1, const double *s2,
+                                           const long long *offsets, long long h, double V,
+                                           double beta, bool want_dp, double *d_h, double *dp,
+                                           double &m, double &t, double &p) {
+  const double c = (double)(offsets[h + 1] - offsets[h]);
+  m = __ddiv_rn(s1[h], c);
+  double rv = __dadd_rn(__ddiv_rn(s2[h], c), -__dmul_rn(m, m));
+  rv = (rv < 0.0) ? 0.0 : rv;   // np.maximum(rv, 0) keeps NaN
+  t = __ddiv_rn(rv, c);
+  const double dh = __dmul_rn(__dsqrt_rn(rv), V);
+  d_h[h] = dh;
+  p = 0.0;
+  if (want_dp) {
+    p = np_scalar_pow(dh, beta);
+    dp[h] = p;
+  }
+}
+
 __global__ void results_leaf_kernel(const double *s1, const double *s2, const long long *offsets,
                                     long long n, double V, double beta, PwPlanDev pw,
                                     double *d_h, double *dp, double *vals, const int *status) {
-  const int leaf = blockIdx.x * blockDim.x + threadIdx.x;
-  if (leaf >= pw.L || (*status & 1)) return;
-  const long long o = pw.leaf_off[leaf];
-  const int len = pw.leaf_len[leaf];
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int leaf = (int)(gt >> 3), j = (int)(gt & 7);
+  if (*status & 1) return;
+  const bool live = leaf < pw.L;
+  const long long o = live ? pw.leaf_off[leaf] : 0;
+  const int len = live ? pw.leaf_len[leaf] : 0;
   const bool want_dp = beta != 0.0;
-  auto elem = [&](long long h, double &m, double &t, double &p) {
-    const double c = (double)(offsets[h + 1] - offsets[h]);
-    m = __ddiv_rn(s1[h], c);
-    double rv = __dadd_rn(__ddiv_rn(s2[h], c), -__dmul_rn(m, m));
-    rv = (rv < 0.0) ? 0.0 : rv;   // np.maximum(rv, 0) keeps NaN
-    t = __ddiv_rn(rv, c);
-    const double dh = __dmul_rn(__dsqrt_rn(rv), V);
-    d_h[h] = dh;
-    p = want_dp ? np_scalar_pow(dh, beta) : 0.0;
-    if (want_dp) dp[h] = p;
-  };
-  double sm, st, sp;
-  if (len < 8) {
-    sm = 0.0; st = 0.0; sp = 0.0;
-    for (int i = 0; i < len; i++) {
+  double rm = 0.0, rt = 0.0, rp = 0.0;
+  const int full = len < 8 ? 0 : len - (len % 8);
+  if (live && len >= 8) {
+    cube_terms(s1, s2, offsets, o + j, V, beta, want_dp, d_h, dp, rm, rt, rp);
+    for (int i = 8 + j; i < full; i += 8) {
       double m, t, p;
-      elem(o + i, m, t, p);
-      sm = __dadd_rn(sm, m); st = __dadd_rn(st, t); sp = __dadd_rn(sp, p);
-    }
-  } else {
-    double rm[8], rt[8], rp[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) elem(o + j, rm[j], rt[j], rp[j]);
-    int i;
-    for (i = 8; i < len - (len % 8); i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        double m, t, p;
-        elem(o + i + j, m, t, p);
-        rm[j] = __dadd_rn(rm[j], m); rt[j] = __dadd_rn(rt[j], t); rp[j] = __dadd_rn(rp[j], p);
-      }
-    }
-    auto tree8 = [](const double *r) {
-      return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                       __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    };
-    sm = tree8(rm); st = tree8(rt); sp = tree8(rp);
-    for (; i < len; i++) {
-      double m, t, p;
-      elem(o + i, m, t, p);
-      sm = __dadd_rn(sm, m); st = __dadd_rn(st, t); sp = __dadd_rn(sp, p);
+      cube_terms(s1, s2, offsets, o + i, V, beta, want_dp, d_h, dp, m, t, p);
+      rm = __dadd_rn(rm, m); rt = __dadd_rn(rt, t); rp = __dadd_rn(rp, p);
     }
   }
-  vals[3 * leaf + 0] = sm;
-  vals[3 * leaf + 1] = st;
-  vals[3 * leaf + 2] = sp;
+#pragma unroll
+  for (int x = 1; x < 8; x <<= 1) {   // pairs, then quads, then halves
+    const double om = __shfl_xor_sync(0xffffffffu, rm, x);
+    const double ot = __shfl_xor_sync(0xffffffffu, rt, x);
+    const double op = __shfl_xor_sync(0xffffffffu, rp, x);
+    rm = __dadd_rn(rm, om); rt = __dadd_rn(rt, ot); rp = __dadd_rn(rp, op);
+  }
+  if (!live || j != 0) return;
+  if (len < 8) { rm = 0.0; rt = 0.0; rp = 0.0; }
+  for (int i = full; i < len; i++) {   // numpy's sequential tail (or n < 8)
+    double m, t, p;
+    cube_terms(s1, s2, offsets, o + i, V, beta, want_dp, d_h, dp, m, t, p);
+    rm = __dadd_rn(rm, m); rt = __dadd_rn(rt, t); rp = __dadd_rn(rp, p);
+  }
+  vals[3 * leaf + 0] = rm;
+  vals[3 * leaf + 1] = rt;
+  vals[3 * leaf + 2] = rp;
 }
 
 // Generic leaf kernel for a plain array (parity entry point vpb_pairwise_sum).
@@ -209,6 +212,7 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
                                  int *status, const long long *explicit_run_base) {
   __shared__ long long buf[PLAN_NT];
   __shared__ long long carry;
+  if (*status) return;   // a failed iteration freezes the plan (error reporting)
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   for (long long b0 = 0; b0 < nb; b0 += PLAN_NT) {
@@ -249,8 +253,10 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
 
 // offsets[h] = exclusive prefix of n_h; tile -> first cube table for the fill.
 __global__ void plan_offsets_kernel(const long long *n_h, long long n, const long long *bpre,
-                                    long long *offsets, const Sched *sched, int *tile_cube) {
+                                    long long *offsets, const Sched *sched, int *tile_cube,
+                                    const int *status) {
   __shared__ long long buf[PLAN_NT];
+  if (status && *status) return;
   const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
   const long long v = h < n ? n_h[h] : 0;
   buf[threadIdx.x] = v;
@@ -310,19 +316,34 @@ __global__ void fill_fixup_kernel(FillArgs a) {
   a.s2[key] = v2;
 }
 
-// Sum the per-CTA histogram slices in CTA order.
+// Sum the per-CTA histogram slices in CTA order (deterministic): block
+// (32 elements x 8 partitions); partition p sums its contiguous range of CTA
+// slices in order, then thread p = 0 adds the 8 partials in order.
 __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
                                    long long m, double *map_w, long long *map_counts) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
+  __shared__ double sw[8][33];
+  __shared__ long long sc[8][33];
+  const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
+  const int p = threadIdx.y;
+  const int per = (nparts + 7) / 8;
+  const int b0 = p * per, b1 = min(nparts, b0 + per);
   double w = 0.0;
   long long c = 0;
-  for (int b = 0; b < nparts; b++) {
-    w = __dadd_rn(w, hw_part[(size_t)b * m + i]);
-    c += hc_part[(size_t)b * m + i];
+  if (i < m)
+    for (int b = b0; b < b1; b++) {
+      w = __dadd_rn(w, hw_part[(size_t)b * m + i]);
+      c += hc_part[(size_t)b * m + i];
+    }
+  sw[p][threadIdx.x] = w;
+  sc[p][threadIdx.x] = c;
+  __syncthreads();
+  if (p == 0 && i < m) {
+    double t = sw[0][threadIdx.x];
+    long long k = sc[0][threadIdx.x];
+    for (int q = 1; q < 8; q++) { t = __dadd_rn(t, sw[q][threadIdx.x]); k += sc[q][threadIdx.x]; }
+    map_w[i] = t;
+    map_counts[i] = k;
   }
-  map_w[i] = w;
-  map_counts[i] = c;
 }
 
 __global__ void hist_glob_convert_kernel(const unsigned long long *hc, long long m,
@@ -332,23 +353,101 @@ __global__ void hist_glob_convert_kernel(const unsigned long long *hc, long long
 }
 
 // --------------------------------------------------------------- refine ----
+// numpy pairwise sum of a shared-memory row of length n <= 4096 by a whole
+// block: thread 0 flattens numpy's split tree into a postfix program (leaf
+// ids and adds), 8 lanes per leaf compute the 8-accumulator leaves, thread 0
+// evaluates the program.  Bit-identical to pw_sum_rt / np.sum.
+struct BlockPw {
+  int n_leaf, n_tok;
+  int leaf_off[32], leaf_len[32];
+  int tok[64];          // >= 0: leaf id, -1: add the two top values
+  double leaf_val[32];
+  double out;
+};
+
+__device__ double block_pairwise(const double *a, int n, BlockPw &S) {
+  if (threadIdx.x == 0) {
+    // explicit-stack post-order walk of numpy's recursion
+    int st_off[16], st_n[16], st_state[16], sp = 0, nl = 0, nt = 0;
+    st_off[0] = 0; st_n[0] = n; st_state[0] = 0;
+    while (sp >= 0) {
+      const int o = st_off[sp], m = st_n[sp];
+      if (m <= 128) {
+        S.leaf_off[nl] = o; S.leaf_len[nl] = m; S.tok[nt++] = nl++;
+        sp--;
+        continue;
+      }
+      int n2 = m / 2; n2 -= n2 % 8;
+      if (st_state[sp] == 0) {
+        st_state[sp] = 1; sp++; st_off[sp] = o; st_n[sp] = n2; st_state[sp] = 0;
+      } else if (st_state[sp] == 1) {
+        st_state[sp] = 2; sp++; st_off[sp] = o + n2; st_n[sp] = m - n2; st_state[sp] = 0;
+      } else {
+        S.tok[nt++] = -1;
+        sp--;
+      }
+    }
+    S.n_leaf = nl; S.n_tok = nt;
+  }
+  __syncthreads();
+  for (int base = 0; base < 8 * S.n_leaf; base += blockDim.x) {
+    const int t = base + threadIdx.x, leaf = t >> 3, j = t & 7;
+    const bool live = leaf < S.n_leaf;
+    const int o = live ? S.leaf_off[leaf] : 0, len = live ? S.leaf_len[leaf] : 0;
+    const int full = len < 8 ? 0 : len - (len % 8);
+    double r = 0.0;
+    if (live && len >= 8) {
+      r = a[o + j];
+      for (int i = 8 + j; i < full; i += 8) r = __dadd_rn(r, a[o + i]);
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, true);
+#pragma unroll
+    for (int x = 1; x < 8; x <<= 1) r = __dadd_rn(r, __shfl_xor_sync(mask, r, x));
+    if (live && j == 0) {
+      if (len < 8) r = 0.0;
+      for (int i = full; i < len; i++) r = __dadd_rn(r, a[o + i]);
+      S.leaf_val[leaf] = r;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double stk[32];
+    int sp = 0;
+    for (int k = 0; k < S.n_tok; k++) {
+      if (S.tok[k] >= 0) stk[sp++] = S.leaf_val[S.tok[k]];
+      else { stk[sp - 2] = __dadd_rn(stk[sp - 2], stk[sp - 1]); sp--; }
+    }
+    S.out = stk[0];
+  }
+  __syncthreads();
+  return S.out;
+}
+
 // One CTA per dimension: smooth_and_damp (vp/maps.py:160-199) then
-// update_grid (vp/maps.py:202-234).  Sequential steps (numpy's pairwise sum
-// and the sequential cumsum) run on one thread to keep numpy's rounding.
-__global__ void refine_kernel(double *edges, const double *map_w, const long long *map_counts,
-                              int ng, double alpha, double *scratch, int *status,
-                              double *damped_out) {
+// update_grid (vp/maps.py:202-234) on a shared-memory copy of the row.
+// numpy's pairwise sums run block-wide (block_pairwise); the cumsum is
+// inherently sequential (numpy's rounding) and runs on one thread.
+constexpr int REFINE_NT = 256;
+constexpr int REFINE_SMEM_NG = 2048;   // rows up to this length live in smem
+
+__global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const double *map_w,
+                                                          const long long *map_counts, int ng,
+                                                          double alpha, double *scratch,
+                                                          int *status, double *damped_out) {
+  extern __shared__ __align__(16) double rsm[];
+  __shared__ BlockPw S;
+  __shared__ int s_skip;
   const int j = blockIdx.x;
-  double *d = scratch + (size_t)j * (5 * ng + 2);
-  double *sm = d + ng;
-  double *dw = sm + ng;
-  double *cum = dw + ng;        // ng+1
-  double *ne = cum + ng + 1;    // new interior edges [1, ng-1]
+  double *d, *sm, *dw, *cum, *ne, *e;
+  if (ng <= REFINE_SMEM_NG) {
+    d = rsm; sm = d + ng; dw = sm + ng; cum = dw + ng; ne = cum + ng + 1; e = ne + ng + 1;
+  } else {
+    d = scratch + (size_t)j * (6 * ng + 3);
+    sm = d + ng; dw = sm + ng; cum = dw + ng; ne = cum + ng + 1; e = ne + ng + 1;
+  }
   const double *w = map_w + (size_t)j * ng;
   const long long *c = map_counts + (size_t)j * ng;
-  double *e = edges + (size_t)j * (ng + 1);
-  __shared__ double s_tot;
-  __shared__ int s_skip;
+  double *eg = edges + (size_t)j * (ng + 1);
   if (*status) return;
   int nz = 0;
   for (int i = threadIdx.x; i < ng; i += blockDim.x) {
@@ -356,31 +455,23 @@ __global__ void refine_kernel(double *edges, const double *map_w, const long lon
     d[i] = v;
     nz |= (v != 0.0);
   }
+  for (int i = threadIdx.x; i <= ng; i += blockDim.x) e[i] = eg[i];
   nz = __syncthreads_or(nz);
-  if (!nz) {
+  auto zero_out = [&]() {
     if (damped_out)
       for (int i = threadIdx.x; i < ng; i += blockDim.x) damped_out[(size_t)j * ng + i] = 0.0;
-    return;
-  }
+  };
+  if (!nz) { zero_out(); return; }
   for (int i = threadIdx.x; i < ng; i += blockDim.x) {
     double v;
     if (i == 0) v = __dadd_rn(__dmul_rn(7.0, d[0]), d[1]);
     else if (i == ng - 1) v = __dadd_rn(d[ng - 2], __dmul_rn(7.0, d[ng - 1]));
     else v = __dadd_rn(__dadd_rn(d[i - 1], __dmul_rn(6.0, d[i])), d[i + 1]);
-    sm[i] = __ddiv_rn(v, 8.0);
+    sm[i] = __dmul_rn(v, 0.125);   // /8.0 (exact power of two)
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    s_tot = pw_sum_rt(sm, ng);
-    s_skip = !(s_tot > 0.0);
-  }
-  __syncthreads();
-  if (s_skip) {
-    if (damped_out)
-      for (int i = threadIdx.x; i < ng; i += blockDim.x) damped_out[(size_t)j * ng + i] = 0.0;
-    return;
-  }
-  const double tot = s_tot;
+  const double tot = ng <= 4096 ? block_pairwise(sm, ng, S) : pw_sum_rt(sm, ng);
+  if (!(tot > 0.0)) { zero_out(); return; }
   for (int i = threadIdx.x; i < ng; i += blockDim.x) {
     const double v = __ddiv_rn(sm[i], tot);
     double r;
@@ -391,17 +482,26 @@ __global__ void refine_kernel(double *edges, const double *map_w, const long lon
     if (damped_out) damped_out[(size_t)j * ng + i] = r;
   }
   __syncthreads();
+  const double tot2 = ng <= 4096 ? block_pairwise(dw, ng, S) : pw_sum_rt(dw, ng);
   if (threadIdx.x == 0) {
-    s_tot = pw_sum_rt(dw, ng);
-    s_skip = !(s_tot > 0.0);
-    if (!s_skip) {
+    s_skip = !(tot2 > 0.0);
+    if (!s_skip) {   // sequential cumsum (np.cumsum)
+      double acc = 0.0;
       cum[0] = 0.0;
-      for (int i = 0; i < ng; i++) cum[i + 1] = __dadd_rn(cum[i], dw[i]);
+      int i = 0;
+      for (; i + 8 <= ng; i += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = dw[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; k++) { acc = __dadd_rn(acc, v[k]); cum[i + k + 1] = acc; }
+      }
+      for (; i < ng; i++) { acc = __dadd_rn(acc, dw[i]); cum[i + 1] = acc; }
     }
   }
   __syncthreads();
   if (s_skip) return;
-  const double delta = __ddiv_rn(s_tot, (double)ng);
+  const double delta = __ddiv_rn(tot2, (double)ng);
   for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) {
     const double goal = __dmul_rn((double)i, delta);
     // searchsorted(cum[1:], goal, 'left'): first iv with cum[iv+1] >= goal
@@ -426,7 +526,11 @@ __global__ void refine_kernel(double *edges, const double *map_w, const long lon
     if (threadIdx.x == 0) atomicOr(status, 2);
     return;
   }
-  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) e[i] = ne[i];
+  for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) eg[i] = ne[i];
+}
+
+inline size_t refine_smem_bytes(int ng) {
+  return ng <= REFINE_SMEM_NG ? sizeof(double) * (6 * (size_t)ng + 3) : 0;
 }
 
 // ---------------------------------------------------------- parity kernels --
