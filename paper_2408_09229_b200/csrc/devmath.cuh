@@ -69,6 +69,45 @@ __device__ __forceinline__ double div_exact(double a, double b, double r) {
   return __fma_rn(e, r, q0);
 }
 
+// ------------------------------------------------ one axis of one sample --
+// vp/kernels.py:67-87 for dimension j of one run:
+//   u = (w>>11)*2^-53, y = RN(RN(digit/N) + RN(u/N)), y >= 1 -> nextafter(1,0),
+//   t = RN(y*ng), iv = min(trunc t, ng-1), frac = RN(t - iv),
+//   x = RN(lo + RN(frac*dx)), jac factor RN(ng*dx).
+// Operation economy (bitwise identical results):
+//  * u/N without materialising u: up = 1 + (bits 11..62 of w)*2^-52 in [1,2)
+//    is pure bit assembly, a = up - (1 - bit63) = 2u exactly (Sterbenz), and
+//    RN(u/N) = RN(a/(2N)) by the Markstein sequence with (2N, RN(1/N)/2) --
+//    the N case scaled by a power of two (tools/proofs/markstein_div.c);
+//  * the y clamp on the bit pattern (y >= 0: y >= 1 iff hi word >= 0x3FF00000);
+//  * trunc(t) by the 2^52 shifter in round-toward-zero, iv clamped in the
+//    integer domain and converted back exactly with the same shifter.
+// dq = RN(digit/N); nsf2 = 2N; rns2 = RN(1/N)/2; e = edges row of the axis.
+__device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2, double rns2,
+                                              double ngf, int ng, const double *e, double &jac,
+                                              int &iv) {
+  const uint32_t whi = (uint32_t)(w >> 32), wlo = (uint32_t)w;
+  const double up = __hiloint2double((int)(((whi >> 11) & 0xFFFFFu) | 0x3FF00000u),
+                                     (int)__funnelshift_r(wlo, whi, 11));
+  const double cm = __hiloint2double((~(int)whi >> 31) & 0x3FF00000, 0);   // 1 - bit63
+  const double a = __dadd_rn(up, -cm);                                      // 2u, exact
+  const double q0 = __dmul_rn(a, rns2);                                     // Markstein
+  const double v = __fma_rn(__fma_rn(-q0, nsf2, a), rns2, q0);             // RN(u/N)
+  const double ys = __dadd_rn(dq, v);
+  int yhi = __double2hiint(ys), ylo = __double2loint(ys);
+  ylo = (yhi >= 0x3FF00000) ? -1 : ylo;                                     // y >= 1 ->
+  yhi = min(yhi, 0x3FEFFFFF);                                               // 0x3FEFFFFFFFFFFFFF
+  const double t = __dmul_rn(__hiloint2double(yhi, ylo), ngf);
+  const int ivj = min(__double2loint(__dadd_rz(t, 4503599627370496.0)), ng - 1);
+  const double fiv = __dadd_rn(__hiloint2double(0x43300000, ivj), -4503599627370496.0);
+  const double frac = __dadd_rn(t, -fiv);
+  const double elo = e[ivj];
+  const double dx = __dadd_rn(e[ivj + 1], -elo);
+  jac = __dmul_rn(jac, __dmul_rn(ngf, dx));
+  iv = ivj;
+  return __dadd_rn(elo, __dmul_rn(frac, dx));
+}
+
 // ------------------------------------------------------------------ exp --
 // exp(x) with < 1 ulp error on the normal range, no table, branch-free:
 // k = rint(x/ln2) via the 1.5*2^52 shifter, two-step Cody-Waite reduction,

@@ -82,12 +82,6 @@ struct FillArgs {
   IParams P;
 };
 
-__device__ __forceinline__ double clamp_below_one(double y) {
-  // if (y >= 1.0) y = nextafter(1, 0): y >= 0, so compare the bit patterns
-  const long long b = __double_as_longlong(y);
-  return __longlong_as_double(b < 0x3FF0000000000000ll ? b : 0x3FEFFFFFFFFFFFFFll);
-}
-
 struct SegItem {   // a partial cube segment (key < 0: none)
   long long key;
   double v1, v2;
@@ -168,6 +162,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   unsigned long long kk = g0 / batch, slot = g0 % batch;
 
   const int lane = tid & 31, warp = tid >> 5;
+  const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
 
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long T0 = lo + tile * FILL_TILE;
@@ -247,24 +242,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
                    w0, w1);
           }
-          const double u = unit_from_word((j & 1) ? w1 : w0);
-          // y >= 1 -> nextafter(1, 0): fmin is exactly that clamp (y is never NaN)
-          const double y = fmin(__dadd_rn(dq[j], div_exact(u, a.nsf, a.rns)),
-                                0.99999999999999988898);
-          const double t = __dmul_rn(y, a.ngf);
-          // trunc(t) for 0 <= t < 2^31 via the 2^52 shifter in round-toward-zero
-          const double sh = __dadd_rz(t, 4503599627370496.0);
-          // iv = min(trunc t, ng-1) and frac = t - iv, branch-free: when t
-          // rounds up to ng (y within ulps of 1) this gives iv = ng-1, frac = 1
-          const int ivj = min(__double2loint(sh), ng - 1);
-          const double frac =
-              __dadd_rn(t, -fmin(__dadd_rn(sh, -4503599627370496.0), a.ngf - 1.0));
-          const double *e = s_edges + j * (ng + 1) + ivj;
-          const double elo = e[0];
-          const double dx = __dadd_rn(e[1], -elo);
-          x[j] = __dadd_rn(elo, __dmul_rn(frac, dx));
-          jac = __dmul_rn(jac, __dmul_rn(a.ngf, dx));
-          iv[j] = ivj;
+          x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
+                             s_edges + j * (ng + 1), jac, iv[j]);
         }
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         const double f = integrand<ID, D>(x, d, a.P);
@@ -284,29 +263,36 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             // most CAS instructions have two lanes on one interval and
             // retry; rotated, a step's lanes are spread over d histograms.
             const int rot = lane % d;
-            int ivr[MAXD];
+            // flat histogram index of each axis, rotated so that slot s holds
+            // axis (s + rot) mod d
+            int idx[MAXD];
 #pragma unroll
-            for (int j = 0; j < (D > 0 ? D : d); j++) ivr[j] = iv[j];
+            for (int j = 0; j < (D > 0 ? D : d); j++) idx[j] = j * ng + iv[j];
             if constexpr (D > 1) {
 #pragma unroll
               for (int b = 1; b < D; b <<= 1) {   // barrel rotation by rot
                 const bool on = (rot & b) != 0;
                 int t[D];
 #pragma unroll
-                for (int j = 0; j < D; j++) t[j] = on ? ivr[(j + b) % D] : ivr[j];
+                for (int j = 0; j < D; j++) t[j] = on ? idx[(j + b) % D] : idx[j];
 #pragma unroll
-                for (int j = 0; j < D; j++) ivr[j] = t[j];
+                for (int j = 0; j < D; j++) idx[j] = t[j];
               }
             } else if constexpr (D == 0) {
+              int ivr[MAXD];
               for (int j = 0; j < d; j++) ivr[j] = iv[(j + rot) % d];
+              for (int j = 0; j < d; j++) idx[j] = ((j + rot) % d) * ng + ivr[j];
             }
-            int jj = rot;
+            // f64: the compiler's LDS -> DADD -> ATOMS.CAST.SPIN loop.  (A
+            // batched variant -- all d reads, adds and value-returning
+            // ATOMS.CAS issued back to back, losers retried -- was measured
+            // 17% slower on cfg2: the value-returning CAS costs more
+            // shared-memory wavefronts than CAST.SPIN and the kernel is
+            // bound by those wavefronts.)
 #pragma unroll
             for (int j = 0; j < (D > 0 ? D : d); j++) {
-              const int idx = jj * ng + ivr[j];
-              atomicAdd(&s_hw[idx], w2);
-              atomicAdd(&s_hc[idx], 1u);
-              jj = (jj + 1 == d) ? 0 : jj + 1;
+              atomicAdd(&s_hw[idx[j]], w2);
+              atomicAdd(&s_hc[idx[j]], 1u);
             }
           } else {
 #pragma unroll

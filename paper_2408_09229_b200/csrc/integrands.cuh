@@ -11,6 +11,10 @@
 #include "devmath.cuh"
 #include "../../include/vegas_b200.h"
 
+#ifndef VPB_MP_UNROLL
+#define VPB_MP_UNROLL 1
+#endif
+
 namespace vpb {
 
 struct IParams {
@@ -51,6 +55,23 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     // p = [n_peaks, sigma, norm, 2 sigma^2, divisor, RN(1/2sigma^2), RN(1/divisor), mu_k...]
     const int np = (int)P.p[0];
     double out = 0.0;
+    if (VPB_MP_UNROLL && np == 3) {
+      // the BASELINE cfg2 case: three independent exp chains, unrolled so
+      // that their FP64 latencies overlap
+      double e[3];
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        double t[MAXD];
+#pragma unroll
+        for (int j = 0; j < (D > 0 ? D : d); j++) {
+          const double u = __dadd_rn(x[j], -P.p[7 + k]);
+          t[j] = __dmul_rn(u, u);
+        }
+        e[k] = __dmul_rn(P.p[2], fast_exp_nonpos(-div_exact(row_sum<D>(t, d), P.p[3], P.p[5])));
+      }
+      out = __dadd_rn(__dadd_rn(__dadd_rn(out, e[0]), e[1]), e[2]);
+      return div_exact(out, P.p[4], P.p[6]);
+    }
     for (int k = 0; k < np; k++) {
       double t[MAXD];
 #pragma unroll

@@ -589,20 +589,11 @@ __global__ void sample_runs_kernel(unsigned long long seed, long long batch, lon
       const unsigned long long blk = base + (unsigned long long)(j >> 1);
       philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K, w0, w1);
     }
-    const double u = unit_from_word((j & 1) ? w1 : w0);
     const long long q = rem / n_strat, dig = rem - q * n_strat;
     rem = q;
-    const double y = clamp_below_one(__dadd_rn(div_exact((double)dig, nsf, rns),
-                                               div_exact(u, nsf, rns)));
-    const double t = __dmul_rn(y, ngf);
-    const double sh = __dadd_rz(t, 4503599627370496.0);
-    int iv = __double2loint(sh);
-    double frac = __dadd_rn(t, -__dadd_rn(sh, -4503599627370496.0));
-    if (iv > ng - 1) { iv = ng - 1; frac = __dadd_rn(t, -(double)(ng - 1)); }
-    const double *e = edges + (size_t)j * (ng + 1) + iv;
-    const double dx = __dadd_rn(e[1], -e[0]);
-    x[i * dims + j] = __dadd_rn(e[0], __dmul_rn(frac, dx));
-    jf = __dmul_rn(jf, __dmul_rn(ngf, dx));
+    int iv;
+    x[i * dims + j] = sample_axis((j & 1) ? w1 : w0, div_exact((double)dig, nsf, rns), 2.0 * nsf,
+                                  0.5 * rns, ngf, ng, edges + (size_t)j * (ng + 1), jf, iv);
     idx[i * dims + j] = iv;
   }
   jac[i] = jf;

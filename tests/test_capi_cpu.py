@@ -84,6 +84,19 @@ def test_magic_division():
         np.testing.assert_array_equal(q, n // np.uint64(D))
 
 
+@pytest.mark.parametrize("src", ["markstein_div.c", "markstein_general.c"])
+def test_division_proofs(tmp_path, src):
+    # The fill kernel's exactly-rounded divisions (devmath.cuh div_exact and
+    # the fused uniform/N form of sample_axis) against IEEE division on the
+    # host FPU (bounded sample; the tools run the full sweep without args).
+    exe = str(tmp_path / "proof")
+    subprocess.run(["gcc", "-O2", "-mfma", "-o", exe, os.path.join(ROOT, "tools", "proofs", src),
+                    "-lm"], check=True)
+    r = subprocess.run([exe, "300"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 mismatches" in r.stdout
+
+
 def test_partition_runs_matches_reference_rule():
     from paper_2408_09229_b200.distributed import partition_runs
     assert partition_runs(10, 3) == [(0, 4), (4, 7), (7, 10)]

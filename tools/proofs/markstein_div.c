@@ -3,7 +3,10 @@
  * returns RN(u/b) for the fill kernel's operands: u = m*2^-53 (m < 2^53
  * integer, the Philox uniform of vp/rng.py:68) and b = n_strat (integer).
  * Also checks the same for u = digit (small integers) and the 2-op
- * reconstruction of u from the 53-bit word.  Build: gcc -O2 -mfma. */
+ * reconstruction of u from the 53-bit word, and the fill kernel's fused form
+ * (devmath.cuh sample_axis): up = 1 + (bits 11..62 of w)*2^-52 assembled from
+ * bits, a = up - (1 - bit63) = 2u exactly, RN(u/b) = Markstein(a, 2b, RN(1/b)/2).
+ * Build: gcc -O2 -mfma. */
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -30,6 +33,15 @@ int main(int argc, char **argv) {
       } else m = xr() >> 11;
       double u = (double)m * 0x1p-53;
       if (mk(m) != u) badu++;
+      { /* fused form from the 64-bit word w = m << 11 | junk, bit63 = top bit of m */
+        uint64_t w = (m << 11) | (xr() & 0x7FF);
+        uint64_t ub = 0x3FF0000000000000ull | ((w >> 11) & ((1ull << 52) - 1));
+        double up; memcpy(&up, &ub, 8);
+        double a = up - ((w >> 63) ? 0.0 : 1.0);
+        double r2 = r * 0.5, b2 = 2.0 * bd;
+        double p0 = a * r2, pe = fma(-p0, b2, a), pq = fma(pe, r2, p0);
+        if (a != 2.0 * u || pq != u / bd) { if (bad < 10) printf("FAIL fused b=%d m=%llu\n", b, (unsigned long long)m); bad++; }
+      }
       double q0 = u * r, e = fma(-q0, bd, u), q = fma(e, r, q0);
       if (q != u / bd) { if (bad < 10) printf("FAIL b=%d m=%llu\n", b, (unsigned long long)m); bad++; }
       n++;
