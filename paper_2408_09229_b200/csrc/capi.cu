@@ -192,6 +192,7 @@ struct vpb_ctx {
   // fill launch geometry
   int grid = 0;
   bool smem_hist = true;
+  bool pairs = false;
   size_t smem = 0;
   // multi-GPU
   int world = 1, rank = 0;
@@ -244,6 +245,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.hw_glob = c->hw_glob;
   a.hc_glob = c->hc_glob;
   a.smem_hist = c->smem_hist ? 1 : 0;
+  a.pairs = c->pairs ? 1 : 0;
   a.status = c->status;
   a.err_run = c->err_run;
   a.P = c->P;
@@ -572,16 +574,24 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+  // layouts in order of preference: pair table + shared histograms (compiled
+  // (id, dims) only), edge rows + shared histograms, edge rows + global
+  // histograms
   c->smem_hist = true;
-  c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1);
+  c->pairs = fill_is_specialised(c->id, c->dims) && !getenv("VPB_NO_PAIRS");
+  c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1, c->pairs);
+  if (c->pairs && c->smem > (size_t)optin) {
+    c->pairs = false;
+    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1, 0);
+  }
   if (c->smem > (size_t)optin) {
     c->smem_hist = false;
-    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0);
+    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0);
   }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
   int per_sm = 0;
-  if (fill_occupancy(c->id, c->dims, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
+  if (fill_occupancy(c->id, c->dims, c->pairs, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
     return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
   c->grid = sms * per_sm;
   if (c->smem_hist) {

@@ -82,9 +82,11 @@ __device__ __forceinline__ double div_exact(double a, double b, double r) {
 //  * the y clamp on the bit pattern (y >= 0: y >= 1 iff hi word >= 0x3FF00000);
 //  * trunc(t) by the 2^52 shifter in round-toward-zero, iv clamped in the
 //    integer domain and converted back exactly with the same shifter.
-// dq = RN(digit/N); nsf2 = 2N; rns2 = RN(1/N)/2; e = edges row of the axis.
+// dq = RN(digit/N); nsf2 = 2N; rns2 = RN(1/N)/2; edge(iv, lo, dx) returns
+// E[j][iv] and RN(E[j][iv+1] - E[j][iv]) of the axis.
+template <class EdgeFn>
 __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2, double rns2,
-                                              double ngf, int ng, const double *e, double &jac,
+                                              double ngf, int ng, EdgeFn edge, double &jac,
                                               int &iv) {
   const uint32_t whi = (uint32_t)(w >> 32), wlo = (uint32_t)w;
   const double up = __hiloint2double((int)(((whi >> 11) & 0xFFFFFu) | 0x3FF00000u),
@@ -101,12 +103,30 @@ __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2
   const int ivj = min(__double2loint(__dadd_rz(t, 4503599627370496.0)), ng - 1);
   const double fiv = __dadd_rn(__hiloint2double(0x43300000, ivj), -4503599627370496.0);
   const double frac = __dadd_rn(t, -fiv);
-  const double elo = e[ivj];
-  const double dx = __dadd_rn(e[ivj + 1], -elo);
+  double elo, dx;
+  edge(ivj, elo, dx);
   jac = __dmul_rn(jac, __dmul_rn(ngf, dx));
   iv = ivj;
   return __dadd_rn(elo, __dmul_rn(frac, dx));
 }
+
+// edge accessors: a row of VegasMap.edges, or a (E[i], RN(E[i+1]-E[i])) pair
+// table precomputed once per fill (one 16-byte shared load per axis)
+struct EdgeRow {
+  const double *e;
+  __device__ __forceinline__ void operator()(int i, double &lo, double &dx) const {
+    lo = e[i];
+    dx = __dadd_rn(e[i + 1], -lo);
+  }
+};
+struct EdgePairs {
+  const double2 *p;
+  __device__ __forceinline__ void operator()(int i, double &lo, double &dx) const {
+    const double2 v = p[i];
+    lo = v.x;
+    dx = v.y;
+  }
+};
 
 // ------------------------------------------------------------------ exp --
 // exp(x) with < 1 ulp error on the normal range, no table, branch-free:

@@ -77,6 +77,7 @@ struct FillArgs {
   double *hw_glob;              // [d*ng] (global-atomic histograms)
   unsigned long long *hc_glob;  // [d*ng]
   int smem_hist;                // 1: CTA-private shared histograms
+  int pairs;                    // 1: (E[i], dx[i]) pair table instead of the edge rows
   int *status;                  // bit0 non-finite, bit1 assert
   unsigned long long *err_run;  // min run index with a non-finite value
   IParams P;
@@ -89,9 +90,10 @@ struct SegItem {   // a partial cube segment (key < 0: none)
 
 // shared-memory layout helper (bytes)
 __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
-                                                  int smem_hist) {
+                                                  int smem_hist, int pairs) {
   size_t b = 0;
-  b += (size_t)dims * (ng + 1) * sizeof(double);                       // edges
+  if (pairs) b += (size_t)dims * ng * 2 * sizeof(double);              // (E[i], dx[i])
+  else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
   if (smem_hist) b += (size_t)dims * ng * (sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
   b += (size_t)FILL_WMAX * sizeof(long long);                          // offsets window
@@ -102,7 +104,11 @@ __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_
   return b;
 }
 
-template <int ID, int D>
+// PAIRS: the map is staged as a table of (E[j][i], RN(E[j][i+1] - E[j][i]))
+// 16-byte pairs, so each axis of a sample costs one LDS.128 instead of two
+// LDS.64 and a DADD (the fill is bound by shared-memory wavefronts; random
+// 16-byte accesses cost ~9 wavefronts per warp vs ~12 for two 8-byte ones).
+template <int ID, int D, bool PAIRS>
 __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
@@ -112,7 +118,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
 
   // ---- shared memory carve-up
   double *s_edges = reinterpret_cast<double *>(smem_raw);
-  size_t off = (size_t)d * (ng + 1) * sizeof(double);
+  double2 *s_pair = reinterpret_cast<double2 *>(smem_raw);
+  size_t off = PAIRS ? (size_t)d * ng * sizeof(double2) : (size_t)d * (ng + 1) * sizeof(double);
   double *s_hw = nullptr;
   unsigned *s_hc = nullptr;
   if (a.smem_hist) {
@@ -141,7 +148,15 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   off += 32 * sizeof(int);
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
 
-  for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
+  if constexpr (PAIRS) {
+    for (int i = tid; i < d * ng; i += FILL_NT) {
+      const int j = i / ng, b = i - j * ng;
+      const double lo = a.edges[j * (ng + 1) + b];
+      s_pair[i] = make_double2(lo, __dadd_rn(a.edges[j * (ng + 1) + b + 1], -lo));
+    }
+  } else {
+    for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
+  }
   if (a.smem_hist)
     for (int i = tid; i < d * ng; i += FILL_NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
   if (dq_tab)
@@ -242,8 +257,12 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
                    w0, w1);
           }
-          x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
-                             s_edges + j * (ng + 1), jac, iv[j]);
+          if constexpr (PAIRS)
+            x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
+                               EdgePairs{s_pair + j * ng}, jac, iv[j]);
+          else
+            x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
+                               EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j]);
         }
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         const double f = integrand<ID, D>(x, d, a.P);

@@ -6,24 +6,25 @@
 namespace vpb {
 
 namespace {
-template <int ID, int D>
+template <int ID, int D, bool PAIRS>
 cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D>,
+    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, PAIRS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  fill_kernel<ID, D><<<grid, FILL_NT, smem, st>>>(a);
+  fill_kernel<ID, D, PAIRS><<<grid, FILL_NT, smem, st>>>(a);
   return cudaGetLastError();
 }
-template <int ID, int D>
+template <int ID, int D, bool PAIRS>
 cudaError_t occ_one(size_t smem, int *ctas) {
-  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D>,
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, PAIRS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D>, FILL_NT, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, PAIRS>, FILL_NT,
+                                                       smem);
 }
 }  // namespace
 
@@ -50,16 +51,23 @@ int fill_is_specialised(int id, int dims) {
 
 cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
                         const FillArgs &a) {
-#define X(I, D) if (id == I && dims == D) return launch_one<I, D>(grid, smem, st, a);
+#define X(I, D)                                                                  \
+  if (id == I && dims == D)                                                      \
+    return a.pairs ? launch_one<I, D, true>(grid, smem, st, a)                   \
+                   : launch_one<I, D, false>(grid, smem, st, a);
   VPB_SPEC_LIST(X)
 #undef X
+  if (a.pairs) return cudaErrorInvalidValue;
   return launch_fill_generic(id, grid, smem, st, a);
 }
 
-cudaError_t fill_occupancy(int id, int dims, size_t smem, int *ctas) {
-#define X(I, D) if (id == I && dims == D) return occ_one<I, D>(smem, ctas);
+cudaError_t fill_occupancy(int id, int dims, int pairs, size_t smem, int *ctas) {
+#define X(I, D)                                                                  \
+  if (id == I && dims == D)                                                      \
+    return pairs ? occ_one<I, D, true>(smem, ctas) : occ_one<I, D, false>(smem, ctas);
   VPB_SPEC_LIST(X)
 #undef X
+  if (pairs) return cudaErrorInvalidValue;
   return fill_occupancy_generic(id, smem, ctas);
 }
 

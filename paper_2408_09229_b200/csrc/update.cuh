@@ -593,7 +593,7 @@ __global__ void sample_runs_kernel(unsigned long long seed, long long batch, lon
     rem = q;
     int iv;
     x[i * dims + j] = sample_axis((j & 1) ? w1 : w0, div_exact((double)dig, nsf, rns), 2.0 * nsf,
-                                  0.5 * rns, ngf, ng, edges + (size_t)j * (ng + 1), jf, iv);
+                                  0.5 * rns, ngf, ng, EdgeRow{edges + (size_t)j * (ng + 1)}, jf, iv);
     idx[i * dims + j] = iv;
   }
   jac[i] = jf;
