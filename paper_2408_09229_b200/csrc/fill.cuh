@@ -88,13 +88,26 @@ struct SegItem {   // a partial cube segment (key < 0: none)
   double v1, v2;
 };
 
+// Row stride of the shared interval histograms, which are laid out
+// [interval][axis] (stride = next power of two >= d, <= 16) rather than the
+// reference's [axis][interval].  Lanes update axes in lane-rotated order, so
+// the lanes of one ATOMS instruction hit distinct axes; with the axis as the
+// fast index their 8-byte (4-byte) words then fall into distinct bank groups
+// except for lanes sharing an axis, which collide with probability
+// 1/(banks per row) -- instead of random interval addresses colliding freely.
+__host__ __device__ inline int hist_stride(int dims) {
+  int s = 1;
+  while (s < dims) s <<= 1;
+  return s <= 16 ? s : dims;
+}
+
 // shared-memory layout helper (bytes)
 __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
                                                   int smem_hist, int pairs) {
   size_t b = 0;
   if (pairs) b += (size_t)dims * ng * 2 * sizeof(double);              // (E[i], dx[i])
   else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
-  if (smem_hist) b += (size_t)dims * ng * (sizeof(double) + sizeof(unsigned));
+  if (smem_hist) b += (size_t)hist_stride(dims) * ng * (sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
   b += (size_t)FILL_WMAX * sizeof(long long);                          // offsets window
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
@@ -115,6 +128,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   const int d = D > 0 ? D : a.dims;
   const int ng = a.ng;
   const int tid = threadIdx.x;
+  const int hs = D > 0 ? hist_stride(D) : hist_stride(a.dims);   // histogram row stride
 
   // ---- shared memory carve-up
   double *s_edges = reinterpret_cast<double *>(smem_raw);
@@ -124,9 +138,9 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   unsigned *s_hc = nullptr;
   if (a.smem_hist) {
     s_hw = reinterpret_cast<double *>(smem_raw + off);
-    off += (size_t)d * ng * sizeof(double);
+    off += (size_t)hs * ng * sizeof(double);
     s_hc = reinterpret_cast<unsigned *>(smem_raw + off);
-    off += (size_t)d * ng * sizeof(unsigned);
+    off += (size_t)hs * ng * sizeof(unsigned);
   }
   off = (off + 15) & ~(size_t)15;
   long long *s_win = reinterpret_cast<long long *>(smem_raw + off);
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
   }
   if (a.smem_hist)
-    for (int i = tid; i < d * ng; i += FILL_NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
+    for (int i = tid; i < hs * ng; i += FILL_NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
   if (dq_tab)
     for (int i = tid; i < a.n_strat; i += FILL_NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
 
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             // axis (s + rot) mod d
             int idx[MAXD];
 #pragma unroll
-            for (int j = 0; j < (D > 0 ? D : d); j++) idx[j] = j * ng + iv[j];
+            for (int j = 0; j < (D > 0 ? D : d); j++) idx[j] = iv[j] * hs + j;
             if constexpr (D > 1) {
 #pragma unroll
               for (int b = 1; b < D; b <<= 1) {   // barrel rotation by rot
@@ -300,7 +314,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             } else if constexpr (D == 0) {
               int ivr[MAXD];
               for (int j = 0; j < d; j++) ivr[j] = iv[(j + rot) % d];
-              for (int j = 0; j < d; j++) idx[j] = ((j + rot) % d) * ng + ivr[j];
+              for (int j = 0; j < d; j++) idx[j] = ivr[j] * hs + (j + rot) % d;
             }
             // f64: the compiler's LDS -> DADD -> ATOMS.CAST.SPIN loop.  (A
             // batched variant -- all d reads, adds and value-returning
@@ -409,7 +423,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     __syncthreads();
     double *hw = a.hw_part + (size_t)blockIdx.x * d * ng;
     unsigned *hc = a.hc_part + (size_t)blockIdx.x * d * ng;
-    for (int i = tid; i < d * ng; i += FILL_NT) { hw[i] = s_hw[i]; hc[i] = s_hc[i]; }
+    for (int i = tid; i < d * ng; i += FILL_NT) {   // back to [axis][interval]
+      const int j = i / ng, b = i - j * ng;
+      hw[i] = s_hw[b * hs + j];
+      hc[i] = s_hc[b * hs + j];
+    }
   }
 }
 
