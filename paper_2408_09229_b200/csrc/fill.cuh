@@ -4,15 +4,20 @@
 // f_batch + kernels.accumulate (vp/executor.py:86-166, vp/kernels.py:36-109)
 // for one rank's run range [lo, hi) of the current plan.
 //
-// Work decomposition: a persistent grid walks tiles of TILE = NT*RPT
-// consecutive runs; each thread owns RPT consecutive runs, so a thread stays
-// inside one hypercube for long stretches and keeps the cube's running sums
-// s1 = sum(jf), s2 = sum(jf^2) in registers.  Cube sums are reduced
-// deterministically and without atomics:
-//   * a cube entirely inside one thread's runs is stored directly;
-//   * a cube spanning threads is closed by a block-wide segmented scan;
+// Work decomposition: the plan's run range is cut into warp tiles of
+// TILE = 32*RPT consecutive runs; each lane owns RPT consecutive runs, so a
+// lane stays inside one hypercube for long stretches and keeps the cube's
+// running sums s1 = sum(jf), s2 = sum(jf^2) in registers.  Cube sums are
+// reduced deterministically and without atomics:
+//   * a cube entirely inside one lane's runs is stored directly;
+//   * a cube spanning lanes is closed by a warp segmented scan (shuffles);
 //   * a cube spanning tiles leaves per-tile carries that fill_fixup_kernel
 //     adds in tile order.
+// The persistent grid's warps are spread over the run range: warp w of CTA b
+// walks tiles w*P + b, w*P + b + grid, ... (P = ntiles / warps-per-CTA), so
+// the warps sharing a CTA's shared histograms sit in distant hypercubes, i.e.
+// in different strata of most axes, and rarely race for the same interval.
+// No block barrier is needed inside the tile loop.
 // Per-dimension interval histograms (MapWeights.w / .counts) live in shared
 // memory (f64 via atom.shared CAS, u32 counts via native ATOMS); each CTA
 // writes its private copy to a slice that hist_reduce_kernel sums in CTA
@@ -38,16 +43,15 @@ namespace vpb {
 #define VPB_FILL_RPT 16
 #endif
 constexpr int FILL_NT = VPB_FILL_NT;    // threads per CTA (one CTA per SM)
-constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per thread per tile
-constexpr int FILL_TILE = FILL_NT * FILL_RPT;
-constexpr int FILL_WMAX = FILL_TILE / 2 + 4;   // cube offsets window per tile
+constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per lane per tile
+constexpr int FILL_TILE = 32 * FILL_RPT;   // runs per warp tile
 constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
 
 // Per-iteration schedule written by the plan kernels (device memory).
 struct Sched {
   long long run_base;     // evaluations consumed by earlier iterations
   long long lo, hi;       // this rank's run range of the plan
-  long long ntiles;       // ceil((hi-lo)/TILE)
+  long long ntiles;       // ceil((hi-lo)/TILE) warp tiles
   long long total;        // plan.total
   long long run_base_next;
   int it;                 // 0-based iteration index being processed
@@ -109,10 +113,7 @@ __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_
   else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
   if (smem_hist) b += (size_t)hist_stride(dims) * ng * (sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
-  b += (size_t)FILL_WMAX * sizeof(long long);                          // offsets window
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
-  b += (size_t)FILL_NT * (2 * sizeof(double) + sizeof(int));           // scan scratch
-  b += 32 * (2 * sizeof(double) + sizeof(int));                        // warp aggregates
   b += 16;                                                              // block flags
   return b;
 }
@@ -143,23 +144,9 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     off += (size_t)hs * ng * sizeof(unsigned);
   }
   off = (off + 15) & ~(size_t)15;
-  long long *s_win = reinterpret_cast<long long *>(smem_raw + off);
-  off += (size_t)FILL_WMAX * sizeof(long long);
   const bool dq_tab = a.n_strat <= DQ_TABLE_MAX;
   double *s_dq = reinterpret_cast<double *>(smem_raw + off);
   off += (dq_tab ? (size_t)a.n_strat : 0) * sizeof(double);
-  double *s_sc1 = reinterpret_cast<double *>(smem_raw + off);
-  off += FILL_NT * sizeof(double);
-  double *s_sc2 = reinterpret_cast<double *>(smem_raw + off);
-  off += FILL_NT * sizeof(double);
-  int *s_scf = reinterpret_cast<int *>(smem_raw + off);
-  off += FILL_NT * sizeof(int);
-  double *s_w1 = reinterpret_cast<double *>(smem_raw + off);
-  off += 32 * sizeof(double);
-  double *s_w2 = reinterpret_cast<double *>(smem_raw + off);
-  off += 32 * sizeof(double);
-  int *s_wf = reinterpret_cast<int *>(smem_raw + off);
-  off += 32 * sizeof(int);
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
 
   if constexpr (PAIRS) {
@@ -185,26 +172,27 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   __syncthreads();
   if (s_flag[0]) return;   // block-uniform
 
-  // (k, slot) of this thread's first run in its first tile; advanced per grid stride
-  unsigned long long g0 = (unsigned long long)(S.run_base + lo + (long long)blockIdx.x * FILL_TILE +
-                                               (long long)tid * FILL_RPT);
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = FILL_NT / 32;
+  const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
+  // this warp's tiles: [w*P + b, min((w+1)*P, ntiles)) in steps of the grid
+  const long long P = (ntiles + NW - 1) / NW;
+  const long long t_beg = (long long)warp * P + blockIdx.x;
+  const long long t_end = min((long long)(warp + 1) * P, ntiles);
+  // (k, slot) of this lane's first run in its first tile; advanced per grid stride
+  unsigned long long g0 = (unsigned long long)(S.run_base + lo + t_beg * FILL_TILE +
+                                               (long long)lane * FILL_RPT);
   unsigned long long kk = g0 / batch, slot = g0 % batch;
 
-  const int lane = tid & 31, warp = tid >> 5;
-  const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
-
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (long long tile = t_beg; tile < t_end; tile += gridDim.x) {
     const long long T0 = lo + tile * FILL_TILE;
     const long long T1 = min(T0 + (long long)FILL_TILE, hi);
     const long long c_first = a.tile_cube[tile];
     const long long c_last = a.tile_cube[tile + 1];
     const int nwin = (int)(c_last - c_first + 2);
-    for (int i = tid; i < nwin; i += FILL_NT) s_win[i] = a.offsets[c_first + i];
-    // no head carry unless a thread below publishes one (after the barriers)
-    if (tid == 0) a.ck_head[tile] = -1;
-    __syncthreads();
+    const long long *win = a.offsets + c_first;   // the tile's cube offsets (L1-resident)
 
-    const long long r0 = T0 + (long long)tid * FILL_RPT;
+    const long long r0 = T0 + (long long)lane * FILL_RPT;
     const long long r1 = min(r0 + (long long)FILL_RPT, T1);
     SegItem H{-1, 0.0, 0.0}, T{-1, 0.0, 0.0};
     int t_through = 0;
@@ -214,11 +202,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       int lo_i = 0, hi_i = nwin - 2;
       while (lo_i < hi_i) {
         const int mid = (lo_i + hi_i + 1) >> 1;
-        if (s_win[mid] <= r0) lo_i = mid; else hi_i = mid - 1;
+        if (__ldg(win + mid) <= r0) lo_i = mid; else hi_i = mid - 1;
       }
       int wi = lo_i;
       long long cube = c_first + wi;
-      long long cube_beg = s_win[wi], cube_end = s_win[wi + 1];
+      long long cube_beg = __ldg(win + wi), cube_end = __ldg(win + wi + 1);
       long long seg_beg = r0;
       double v1 = 0.0, v2 = 0.0;
       unsigned long long k = kk, sl = slot;
@@ -250,10 +238,10 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       for (long long r = r0; r < r1; r++) {
         if (r >= cube_end) {
           close_segment(r);
-          do { wi++; } while (s_win[wi + 1] <= r);
+          do { wi++; } while (__ldg(win + wi + 1) <= r);
           cube = c_first + wi;
-          cube_beg = s_win[wi];
-          cube_end = s_win[wi + 1];
+          cube_beg = __ldg(win + wi);
+          cube_end = __ldg(win + wi + 1);
           seg_beg = r;
           v1 = 0.0; v2 = 0.0;
           load_digits(cube);
@@ -340,7 +328,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       close_segment(r1);
     }
 
-    // ---- block segmented scan of the tail items (chain values flow forward)
+    // ---- warp segmented scan of the tail items (chain values flow forward)
     // element: (flag = chain restarts here, v); flag=1 also for "no tail".
     int fl = (T.key < 0) ? 1 : (t_through ? 0 : 1);
     double e1 = T.key < 0 ? 0.0 : T.v1, e2 = T.key < 0 ? 0.0 : T.v2;
@@ -352,71 +340,47 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       if (lane >= o && !fl) { e1 = __dadd_rn(p1, e1); e2 = __dadd_rn(p2, e2); }
       if (lane >= o) fl |= pf;
     }
-    if (lane == 31) { s_w1[warp] = e1; s_w2[warp] = e2; s_wf[warp] = fl; }
-    __syncthreads();
-    if (warp == 0) {
-      constexpr int NW = FILL_NT / 32;
-      int wf = lane < NW ? s_wf[lane] : 1;
-      double a1 = lane < NW ? s_w1[lane] : 0.0, a2 = lane < NW ? s_w2[lane] : 0.0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int pf = __shfl_up_sync(0xffffffffu, wf, o);
-        const double p1 = __shfl_up_sync(0xffffffffu, a1, o);
-        const double p2 = __shfl_up_sync(0xffffffffu, a2, o);
-        if (lane >= o && !wf) { a1 = __dadd_rn(p1, a1); a2 = __dadd_rn(p2, a2); }
-        if (lane >= o) wf |= pf;
-      }
-      if (lane < NW) { s_w1[lane] = a1; s_w2[lane] = a2; s_wf[lane] = wf; }
-    }
-    __syncthreads();
-    // rooted: does the inclusive chain of this thread contain a restart inside the tile?
-    int rooted = fl;
-    if (warp > 0 && !fl) {
-      e1 = __dadd_rn(s_w1[warp - 1], e1);
-      e2 = __dadd_rn(s_w2[warp - 1], e2);
-      rooted = s_wf[warp - 1];
-    }
-    s_sc1[tid] = e1;
-    s_sc2[tid] = e2;
-    s_scf[tid] = rooted;
-    __syncthreads();
-    // ---- heads close chains
+    // fl is now "rooted": the inclusive chain has a restart inside the tile
+    const int pfl = __shfl_up_sync(0xffffffffu, fl, 1);
+    const double pe1 = __shfl_up_sync(0xffffffffu, e1, 1);
+    const double pe2 = __shfl_up_sync(0xffffffffu, e2, 1);
+    // ---- heads close chains; the one whose chain began before the tile
+    // (lane 0's head, or a head after an unrooted chain) is the head carry
+    bool head_carry = false;
+    double h1 = H.v1, h2 = H.v2;
     if (H.key >= 0) {
-      if (tid == 0) {
-        a.ck_head[tile] = H.key;
-        a.cv_head[2 * tile] = H.v1;
-        a.cv_head[2 * tile + 1] = H.v2;
+      if (lane > 0) { h1 = __dadd_rn(pe1, H.v1); h2 = __dadd_rn(pe2, H.v2); }
+      if (lane > 0 && pfl) {
+        a.s1[H.key] = h1;
+        a.s2[H.key] = h2;
       } else {
-        const double t1 = __dadd_rn(s_sc1[tid - 1], H.v1);
-        const double t2 = __dadd_rn(s_sc2[tid - 1], H.v2);
-        if (s_scf[tid - 1]) {
-          a.s1[H.key] = t1;
-          a.s2[H.key] = t2;
-        } else {
-          a.ck_head[tile] = H.key;
-          a.cv_head[2 * tile] = t1;
-          a.cv_head[2 * tile + 1] = t2;
-        }
+        head_carry = true;
       }
     }
-    // ---- the tile's last thread with runs publishes the tail carry
+    if (head_carry) {
+      a.ck_head[tile] = H.key;
+      a.cv_head[2 * tile] = h1;
+      a.cv_head[2 * tile + 1] = h2;
+    }
+    const unsigned any_head = __ballot_sync(0xffffffffu, head_carry);
+    if (lane == 0 && any_head == 0) a.ck_head[tile] = -1;
+    // ---- the tile's last lane with runs publishes the tail carry
     const int last = (int)((T1 - T0 + FILL_RPT - 1) / FILL_RPT) - 1;
-    if (tid == last) {
+    if (lane == last) {
       if (T.key >= 0) {
         a.ck_tail[tile] = T.key;
         a.cv_tail[2 * tile] = e1;
         a.cv_tail[2 * tile + 1] = e2;
-        a.ct_through[tile] = rooted ? 0 : 1;
+        a.ct_through[tile] = fl ? 0 : 1;
       } else {
         a.ck_tail[tile] = -1;
         a.ct_through[tile] = 0;
       }
     }
-    // advance this thread's RNG coordinates by one grid stride of tiles
+    // advance this lane's RNG coordinates by one grid stride of tiles
     kk += (unsigned long long)a.dk;
     slot += (unsigned long long)a.ds;
     if (slot >= batch) { slot -= batch; kk++; }
-    __syncthreads();   // s_win / scan scratch reused by the next tile
   }
 
   if (a.smem_hist) {
