@@ -88,7 +88,7 @@ struct FillArgs {
 };
 
 struct SegItem {   // a partial cube segment (key < 0: none)
-  long long key;
+  int key;
   double v1, v2;
 };
 
@@ -204,14 +204,18 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
         const int mid = (lo_i + hi_i + 1) >> 1;
         if (__ldg(win + mid) <= r0) lo_i = mid; else hi_i = mid - 1;
       }
+      // run positions relative to r0 in 32-bit registers (cube bounds clamped
+      // to [-1, RPT+1], which keeps every comparison below exact)
+      auto rel = [&](long long v) { return (int)max(min(v - r0, (long long)FILL_RPT + 1), -1ll); };
+      const int n = (int)(r1 - r0);
       int wi = lo_i;
-      long long cube = c_first + wi;
-      long long cube_beg = __ldg(win + wi), cube_end = __ldg(win + wi + 1);
-      long long seg_beg = r0;
+      int cube = (int)c_first + wi;
+      int cb = rel(__ldg(win + wi)), ce = rel(__ldg(win + wi + 1));
+      int seg_beg = 0;
       double v1 = 0.0, v2 = 0.0;
       unsigned long long k = kk, sl = slot;
       double dq[MAXD];
-      auto load_digits = [&](long long c) {
+      auto load_digits = [&](int c) {
         uint32_t rem = (uint32_t)c;   // n_cubes < 2^31
 #pragma unroll
         for (int j = 0; j < (D > 0 ? D : d); j++) {
@@ -221,9 +225,9 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
         }
       };
-      auto close_segment = [&](long long seg_end) {
-        const bool before = cube_beg < seg_beg;   // cube started before this thread
-        const bool after = cube_end > seg_end;    // cube continues past this thread
+      auto close_segment = [&](int seg_end) {
+        const bool before = cb < seg_beg;   // cube started before this lane
+        const bool after = ce > seg_end;    // cube continues past this lane
         if (!before && !after) {
           a.s1[cube] = v1;
           a.s2[cube] = v2;
@@ -235,19 +239,20 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
         }
       };
       load_digits(cube);
-      for (long long r = r0; r < r1; r++) {
-        if (r >= cube_end) {
-          close_segment(r);
-          do { wi++; } while (__ldg(win + wi + 1) <= r);
-          cube = c_first + wi;
-          cube_beg = __ldg(win + wi);
-          cube_end = __ldg(win + wi + 1);
-          seg_beg = r;
+      // Philox block of this run's first axis pair: k*stride/2 (vp/kernels.py:59-66)
+      unsigned long long base = k * stride_half;
+      for (int rr = 0; rr < n; rr++) {
+        if (rr >= ce) {
+          close_segment(rr);
+          do { wi++; } while (__ldg(win + wi + 1) <= r0 + rr);
+          cube = (int)c_first + wi;
+          cb = rel(__ldg(win + wi));
+          ce = rel(__ldg(win + wi + 1));
+          seg_beg = rr;
           v1 = 0.0; v2 = 0.0;
           load_digits(cube);
         }
         // ---- sample (vp/kernels.py:59-88)
-        const unsigned long long base = k * stride_half;
         double x[MAXD];
         int iv[MAXD];
         double jac = 1.0;
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         const double f = integrand<ID, D>(x, d, a.P);
         if (!isfinite(f)) {
-          atomicMin(a.err_run, (unsigned long long)r);
+          atomicMin(a.err_run, (unsigned long long)(r0 + rr));
           atomicOr(a.status, 1);
         } else {
           const double jf = __dmul_rn(jac, f);
@@ -323,9 +328,9 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             }
           }
         }
-        if (++sl == batch) { sl = 0; k++; }
+        if (++sl == batch) { sl = 0; base += stride_half; }
       }
-      close_segment(r1);
+      close_segment(n);
     }
 
     // ---- warp segmented scan of the tail items (chain values flow forward)
