@@ -24,6 +24,7 @@
 #include "../../include/vegas_b200.h"
 #include "fill_launch.h"
 #include "update.cuh"
+#include "hist.cuh"
 
 using namespace vpb;
 
@@ -194,6 +195,14 @@ struct vpb_ctx {
   bool smem_hist = true;
   bool pairs = false;
   size_t smem = 0;
+  // records mode (histograms too large for shared memory): chunked fill ->
+  // hist_records_kernel per 8-axis group
+  bool records = false;
+  long long rec_ch = 0;        // runs per chunk (multiple of FILL_TILE)
+  int n_chunks = 0, n_groups = 0, rec_B = 0;
+  unsigned short *rec_iv = nullptr;
+  double *rec_w2 = nullptr, *hw_rec = nullptr;
+  unsigned *hc_rec = nullptr;
   // multi-GPU
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -246,6 +255,14 @@ FillArgs fill_args(vpb_ctx *c) {
   a.hc_glob = c->hc_glob;
   a.smem_hist = c->smem_hist ? 1 : 0;
   a.pairs = c->pairs ? 1 : 0;
+  a.records = c->records ? 1 : 0;
+  a.tile_lo = 0;
+  a.tile_hi = (long long)1 << 62;
+  a.rec_iv = c->rec_iv;
+  a.rec_w2 = c->rec_w2;
+  a.rec_ch = c->rec_ch;
+  a.dig_bits = 0;
+  while ((1ll << a.dig_bits) < c->ns) a.dig_bits++;
   a.status = c->status;
   a.err_run = c->err_run;
   a.P = c->P;
@@ -279,19 +296,48 @@ int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
 int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr) {
   const size_t m = (size_t)c->dims * c->ng;
   CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
-  if (!c->smem_hist) {
+  if (!c->smem_hist && !c->records) {
     CK(cudaMemsetAsync(c->hw_glob, 0, sizeof(double) * m, c->st));
     CK(cudaMemsetAsync(c->hc_glob, 0, sizeof(unsigned long long) * m, c->st));
   }
   FillArgs a = fill_args(c);
   if (timed) CK(cudaEventRecord(c->f0, c->st));
   if (k0) CK(rec_event(c, k0));
-  CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+  if (!c->records) {
+    CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+  } else {
+    // chunks of rec_ch runs: fill (records) -> per-group shared histograms
+    const long long tpc = c->rec_ch / FILL_TILE;
+    for (int ch = 0; ch < c->n_chunks; ch++) {
+      a.tile_lo = ch * tpc;
+      a.tile_hi = (ch + 1) * tpc;
+      CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+      for (int g = 0; g < c->n_groups; g++) {
+        const int jn = std::min(8, c->dims - 8 * g);
+        const size_t goff = (size_t)g * c->rec_B * c->ng * 8;
+        const size_t sm = hist_records_smem(c->ng);
+#define VPB_HR(J)                                                                           \
+  case J:                                                                                   \
+    hist_records_kernel<J><<<c->rec_B, HR_NT, sm, c->st>>>(                                 \
+        c->rec_iv, c->rec_w2, c->rec_ch, a.tile_lo, c->sched, c->ng, g, c->hw_rec + goff,   \
+        c->hc_rec + goff, ch == 0, c->status);                                              \
+    break;
+        switch (jn) {
+          VPB_HR(1) VPB_HR(2) VPB_HR(3) VPB_HR(4) VPB_HR(5) VPB_HR(6) VPB_HR(7) VPB_HR(8)
+        }
+#undef VPB_HR
+      }
+    }
+    CK(cudaGetLastError());
+  }
   if (k1) CK(rec_event(c, k1));
   if (timed) CK(cudaEventRecord(c->f1, c->st));
   const long long nt = c->ntiles_cap;
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
-  if (c->smem_hist) {
+  if (c->records) {
+    rec_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
+        c->hw_rec, c->hc_rec, c->rec_B, c->dims, c->ng, c->map_w, c->map_counts, c->status);
+  } else if (c->smem_hist) {
     hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
         c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
   } else {
@@ -435,7 +481,7 @@ void free_ctx(vpb_ctx *c) {
                   c->pwvals, c->sched, c->sc, c->h_est, c->h_var, c->h_evals, c->tile_cube,
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
-                  c->refine_scr, c->explicit_rb};
+                  c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   c->pw.release();
@@ -577,8 +623,12 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // layouts in order of preference: pair table + shared histograms (compiled
   // (id, dims) only), edge rows + shared histograms, edge rows + global
   // histograms
-  c->smem_hist = true;
-  c->pairs = fill_is_specialised(c->id, c->dims) && !getenv("VPB_NO_PAIRS");
+  // VPB_FILL_LAYOUT=records|global|edges forces a layout (tests, A/B)
+  const char *force = std::getenv("VPB_FILL_LAYOUT");
+  const std::string forced = force ? force : "";
+  c->smem_hist = forced != "records" && forced != "global";
+  c->pairs = c->smem_hist && forced != "edges" && fill_is_specialised(c->id, c->dims) &&
+             !getenv("VPB_NO_PAIRS");
   c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1, c->pairs);
   if (c->pairs && c->smem > (size_t)optin) {
     c->pairs = false;
@@ -590,11 +640,47 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
+  // histograms too large for shared memory: records mode (chunked fill +
+  // shared-memory histograms per 8-axis group), else global atomics
+  c->records = !c->smem_hist && forced != "global" && c->ng <= 65535 &&
+               hist_records_smem(c->ng) <= (size_t)optin;
+  const bool spec = fill_is_specialised(c->id, c->dims);
+  const int layout = (c->records && spec)     ? LAYOUT_RECORDS
+                     : c->pairs               ? LAYOUT_PAIRS
+                     : (c->smem_hist && spec) ? LAYOUT_EDGES
+                                              : LAYOUT_RUNTIME;
   int per_sm = 0;
-  if (fill_occupancy(c->id, c->dims, c->pairs, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
+  if (fill_occupancy(c->id, c->dims, layout, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
     return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
   c->grid = sms * per_sm;
-  if (c->smem_hist) {
+  if (c->records) {
+    c->n_groups = (c->dims + 7) / 8;
+    const long long cap_runs = c->ntiles_cap * FILL_TILE;
+    const long long per_rec = 8 + 16 * (long long)c->n_groups;
+    long long ch = (4ll << 30) / per_rec;   // <= 4 GiB of records per chunk
+    if (const char *e = std::getenv("VPB_REC_CHUNK")) ch = std::max(1ll, std::atoll(e));
+    ch -= ch % FILL_TILE;
+    if (ch < FILL_TILE) ch = FILL_TILE;
+    c->rec_ch = std::min(ch, cap_runs);
+    c->n_chunks = (int)((cap_runs + c->rec_ch - 1) / c->rec_ch);
+    const size_t hsm = hist_records_smem(c->ng);
+    int hr_per_sm = 0;
+#define VPB_HR_ATTR(J)                                                                        \
+  if (cudaFuncSetAttribute(hist_records_kernel<J>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)hsm) != cudaSuccess)                                           \
+    return bail(fail(VPB_ERR_CUDA, "hist_records smem attribute"));
+    VPB_HR_ATTR(1) VPB_HR_ATTR(2) VPB_HR_ATTR(3) VPB_HR_ATTR(4)
+    VPB_HR_ATTR(5) VPB_HR_ATTR(6) VPB_HR_ATTR(7) VPB_HR_ATTR(8)
+#undef VPB_HR_ATTR
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hr_per_sm, hist_records_kernel<8>, HR_NT,
+                                                      hsm) != cudaSuccess || hr_per_sm < 1)
+      return bail(fail(VPB_ERR_CUDA, "hist_records kernel cannot be resident"));
+    c->rec_B = std::max(1, (sms * hr_per_sm + c->n_groups - 1) / c->n_groups);
+    A(c->rec_iv, (size_t)c->n_groups * c->rec_ch * 8);
+    A(c->rec_w2, (size_t)c->rec_ch);
+    A(c->hw_rec, (size_t)c->n_groups * c->rec_B * c->ng * 8);
+    A(c->hc_rec, (size_t)c->n_groups * c->rec_B * c->ng * 8);
+  } else if (c->smem_hist) {
     A(c->hw_part, (size_t)c->grid * m);
     A(c->hc_part, (size_t)c->grid * m);
   } else {

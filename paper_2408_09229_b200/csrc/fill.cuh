@@ -81,6 +81,12 @@ struct FillArgs {
   double *hw_glob;              // [d*ng] (global-atomic histograms)
   unsigned long long *hc_glob;  // [d*ng]
   int smem_hist;                // 1: CTA-private shared histograms
+  int records;                  // 1: write (interval, w^2) records for hist_records_kernel
+  int dig_bits;                 // bits per packed cube digit (d > 12 kernels)
+  long long tile_lo, tile_hi;   // tiles of this launch (records mode: one chunk)
+  unsigned short *rec_iv;       // [n_groups][rec_ch][8] intervals, axes 8g..8g+7
+  double *rec_w2;               // [rec_ch]
+  long long rec_ch;             // records per chunk (a multiple of FILL_TILE)
   int pairs;                    // 1: (E[i], dx[i]) pair table instead of the edge rows
   int *status;                  // bit0 non-finite, bit1 assert
   unsigned long long *err_run;  // min run index with a non-finite value
@@ -122,8 +128,19 @@ __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_
 // 16-byte pairs, so each axis of a sample costs one LDS.128 instead of two
 // LDS.64 and a DADD (the fill is bound by shared-memory wavefronts; random
 // 16-byte accesses cost ~9 wavefronts per warp vs ~12 for two 8-byte ones).
-template <int ID, int D, bool PAIRS>
+// Kernel layouts (compile time for the (integrand, dims) specialisations;
+// LAYOUT_RUNTIME reads the FillArgs flags).
+constexpr int LAYOUT_EDGES = 0;     // edge rows + shared histograms
+constexpr int LAYOUT_PAIRS = 1;     // pair table + shared histograms
+constexpr int LAYOUT_RECORDS = 2;   // edge rows + records (hist.cuh)
+constexpr int LAYOUT_RUNTIME = 3;   // generic kernel: a.smem_hist / a.records / global atomics
+
+template <int ID, int D, int LAYOUT>
 __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
+  constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
+  // cube digits RN(digit/N) per axis in registers for small d; above that the
+  // digits are kept packed and RN(digit/N) is read from the shared table
+  constexpr bool DQ_REG = D == 0 || D <= 12;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
@@ -147,6 +164,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   const bool dq_tab = a.n_strat <= DQ_TABLE_MAX;
   double *s_dq = reinterpret_cast<double *>(smem_raw + off);
   off += (dq_tab ? (size_t)a.n_strat : 0) * sizeof(double);
+  const int dbits = a.dig_bits;                 // bits per packed digit (!DQ_REG)
+  const uint64_t dmask = (1ull << dbits) - 1;
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
 
   if constexpr (PAIRS) {
@@ -175,10 +194,13 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = FILL_NT / 32;
   const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
-  // this warp's tiles: [w*P + b, min((w+1)*P, ntiles)) in steps of the grid
-  const long long P = (ntiles + NW - 1) / NW;
-  const long long t_beg = (long long)warp * P + blockIdx.x;
-  const long long t_end = min((long long)(warp + 1) * P, ntiles);
+  // this warp's tiles: [L + w*P + b, min(L + (w+1)*P, U)) in steps of the grid,
+  // [L, U) = the launch's tile range
+  const long long tL = a.tile_lo, tU = min(a.tile_hi, ntiles);
+  const long long P = (tU - tL + NW - 1) / NW;
+  const long long t_beg = tL + (long long)warp * P + blockIdx.x;
+  const long long t_end = min(tL + (long long)(warp + 1) * P, tU);
+  const long long rec0 = lo + tL * FILL_TILE;   // run of record 0 (records mode)
   // (k, slot) of this lane's first run in its first tile; advanced per grid stride
   unsigned long long g0 = (unsigned long long)(S.run_base + lo + t_beg * FILL_TILE +
                                                (long long)lane * FILL_RPT);
@@ -214,15 +236,27 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
       int seg_beg = 0;
       double v1 = 0.0, v2 = 0.0;
       unsigned long long k = kk, sl = slot;
-      double dq[MAXD];
+      double dq[DQ_REG ? MAXD : 1];
+      uint64_t dpk = 0;   // packed digits (!DQ_REG)
       auto load_digits = [&](int c) {
         uint32_t rem = (uint32_t)c;   // n_cubes < 2^31
+        if constexpr (!DQ_REG) dpk = 0;
 #pragma unroll
         for (int j = 0; j < (D > 0 ? D : d); j++) {
           const uint32_t q = a.nsdiv.div(rem);
           const uint32_t dig = rem - q * a.nsdiv.d;
           rem = q;
-          dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
+          if constexpr (DQ_REG) dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
+          else dpk |= (uint64_t)dig << (j * dbits);
+        }
+      };
+      // RN(digit_j / N) of the current cube
+      auto dq_of = [&](int j) -> double {
+        if constexpr (DQ_REG) {
+          return dq[j];
+        } else {
+          const uint32_t dig = (uint32_t)((dpk >> (j * dbits)) & dmask);
+          return s_dq[dig];
         }
       };
       auto close_segment = [&](int seg_end) {
@@ -265,11 +299,28 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
                    w0, w1);
           }
           if constexpr (PAIRS)
-            x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
+            x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
                                EdgePairs{s_pair + j * ng}, jac, iv[j]);
           else
-            x[j] = sample_axis((j & 1) ? w1 : w0, dq[j], nsf2, rns2, a.ngf, ng,
+            x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
                                EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j]);
+          if constexpr (LAYOUT == LAYOUT_RECORDS) {
+            // the axis group is complete: store its intervals now, so they
+            // are not live across the integrand
+            if ((j & 7) == 7 || j == D - 1) {
+              const int g = j >> 3;
+              uint32_t wv[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const int j0 = 8 * g + 2 * q, j1 = j0 + 1;
+                const uint32_t lo16 = j0 <= j ? (uint32_t)iv[j0 <= j ? j0 : 0] : 0u;
+                const uint32_t hi16 = j1 <= j ? (uint32_t)iv[j1 <= j ? j1 : 0] : 0u;
+                wv[q] = lo16 | (hi16 << 16);
+              }
+              *reinterpret_cast<uint4 *>(a.rec_iv + ((size_t)g * a.rec_ch + (r0 + rr - rec0)) * 8) =
+                  make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          }
         }
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         const double f = integrand<ID, D>(x, d, a.P);
@@ -282,7 +333,30 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           v1 = __dadd_rn(v1, jf);
           v2 = __dadd_rn(v2, w2);
           // ---- interval histograms (vp/kernels.py:100-105)
-          if (a.smem_hist) {
+          constexpr bool RT = LAYOUT == LAYOUT_RUNTIME;
+          if (LAYOUT == LAYOUT_RECORDS) {
+            a.rec_w2[r0 + rr - rec0] = w2;   // intervals were stored while sampling
+          } else if (RT && a.records) {
+            // deferred to hist_records_kernel: w^2 and the intervals, 8 axes
+            // per 16-byte group (coalesced over a warp's RPT-strided rows)
+            const long long ri = r0 + rr - rec0;
+            a.rec_w2[ri] = w2;
+            constexpr int NG = (MAXD + 7) / 8;
+#pragma unroll
+            for (int g = 0; g < NG; g++) {
+              if (D == 0 && 8 * g >= d) break;
+              uint32_t wv[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const int j0 = 8 * g + 2 * q, j1 = j0 + 1;
+                const uint32_t lo16 = (D > 0 ? j0 < D : j0 < d) ? (uint32_t)iv[j0 < MAXD ? j0 : 0] : 0u;
+                const uint32_t hi16 = (D > 0 ? j1 < D : j1 < d) ? (uint32_t)iv[j1 < MAXD ? j1 : 0] : 0u;
+                wv[q] = lo16 | (hi16 << 16);
+              }
+              *reinterpret_cast<uint4 *>(a.rec_iv + ((size_t)g * a.rec_ch + ri) * 8) =
+                  make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          } else if (!RT || a.smem_hist) {
             // Lane-rotated dimension order: at step s lane l updates dim
             // (s + l) mod d.  Lanes of a warp usually sit in the same cube,
             // i.e. the same stratum of every axis, so with a common order

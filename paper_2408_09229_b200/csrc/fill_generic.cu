@@ -8,20 +8,20 @@ template <int ID>
 cudaError_t launch_g(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, 0, false>,
+    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, 0, LAYOUT_RUNTIME>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  fill_kernel<ID, 0, false><<<grid, FILL_NT, smem, st>>>(a);
+  fill_kernel<ID, 0, LAYOUT_RUNTIME><<<grid, FILL_NT, smem, st>>>(a);
   return cudaGetLastError();
 }
 template <int ID>
 cudaError_t occ_g(size_t smem, int *ctas) {
-  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, 0, false>,
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, 0, LAYOUT_RUNTIME>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, 0, false>, FILL_NT, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, 0, LAYOUT_RUNTIME>, FILL_NT, smem);
 }
 }  // namespace
 

@@ -9,11 +9,12 @@ namespace vpb {
 // Launch the fill kernel for (id, dims).  Uses the compile-time-dims kernel
 // when one is instantiated (fill_spec.cu), else the generic runtime-dims one
 // (fill_generic.cu).  `grid` CTAs of FILL_NT threads, `smem` dynamic bytes.
-// a.pairs selects the pair-table kernel (specialised (id, dims) only).
+// a.records / a.pairs / a.smem_hist select the layout of a specialised
+// (id, dims) kernel; global-atomic histograms use the generic kernel.
 cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
                         const FillArgs &a);
 // CTAs per SM the chosen kernel can keep resident with `smem` bytes.
-cudaError_t fill_occupancy(int id, int dims, int pairs, size_t smem, int *ctas_per_sm);
+cudaError_t fill_occupancy(int id, int dims, int layout, size_t smem, int *ctas_per_sm);
 // 1 if (id, dims) has a compile-time specialisation.
 int fill_is_specialised(int id, int dims);
 

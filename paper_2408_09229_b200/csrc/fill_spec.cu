@@ -6,24 +6,24 @@
 namespace vpb {
 
 namespace {
-template <int ID, int D, bool PAIRS>
+template <int ID, int D, int LAYOUT>
 cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, PAIRS>,
+    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  fill_kernel<ID, D, PAIRS><<<grid, FILL_NT, smem, st>>>(a);
+  fill_kernel<ID, D, LAYOUT><<<grid, FILL_NT, smem, st>>>(a);
   return cudaGetLastError();
 }
-template <int ID, int D, bool PAIRS>
+template <int ID, int D, int LAYOUT>
 cudaError_t occ_one(size_t smem, int *ctas) {
-  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, PAIRS>,
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, PAIRS>, FILL_NT,
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, LAYOUT>, FILL_NT,
                                                        smem);
 }
 }  // namespace
@@ -52,22 +52,27 @@ int fill_is_specialised(int id, int dims) {
 cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
                         const FillArgs &a) {
 #define X(I, D)                                                                  \
-  if (id == I && dims == D)                                                      \
-    return a.pairs ? launch_one<I, D, true>(grid, smem, st, a)                   \
-                   : launch_one<I, D, false>(grid, smem, st, a);
+  if (id == I && dims == D) {                                                    \
+    if (a.records) return launch_one<I, D, LAYOUT_RECORDS>(grid, smem, st, a);   \
+    if (a.pairs) return launch_one<I, D, LAYOUT_PAIRS>(grid, smem, st, a);       \
+    if (a.smem_hist) return launch_one<I, D, LAYOUT_EDGES>(grid, smem, st, a);   \
+  }
   VPB_SPEC_LIST(X)
 #undef X
   if (a.pairs) return cudaErrorInvalidValue;
-  return launch_fill_generic(id, grid, smem, st, a);
+  return launch_fill_generic(id, grid, smem, st, a);   // incl. global-atomic histograms
 }
 
-cudaError_t fill_occupancy(int id, int dims, int pairs, size_t smem, int *ctas) {
+cudaError_t fill_occupancy(int id, int dims, int layout, size_t smem, int *ctas) {
 #define X(I, D)                                                                  \
-  if (id == I && dims == D)                                                      \
-    return pairs ? occ_one<I, D, true>(smem, ctas) : occ_one<I, D, false>(smem, ctas);
+  if (id == I && dims == D && layout != LAYOUT_RUNTIME) {                        \
+    if (layout == LAYOUT_RECORDS) return occ_one<I, D, LAYOUT_RECORDS>(smem, ctas); \
+    if (layout == LAYOUT_PAIRS) return occ_one<I, D, LAYOUT_PAIRS>(smem, ctas);  \
+    return occ_one<I, D, LAYOUT_EDGES>(smem, ctas);                              \
+  }
   VPB_SPEC_LIST(X)
 #undef X
-  if (pairs) return cudaErrorInvalidValue;
+  if (layout == LAYOUT_PAIRS) return cudaErrorInvalidValue;
   return fill_occupancy_generic(id, smem, ctas);
 }
 

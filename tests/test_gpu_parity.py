@@ -186,6 +186,22 @@ def test_fill_matches_oracle(name, dims, ng, ns, nh):
     np.testing.assert_allclose(got[3], ref[3], rtol=1e-12, atol=1e-290)
 
 
+@pytest.mark.parametrize("layout,chunk", [("records", "2048"), ("records", ""), ("global", "")])
+@pytest.mark.parametrize("name,dims,ng,ns,nh", [
+    ("gaussian20", 20, 64, 1, (5000, 5001)),     # 3 axis groups (8, 8, 4)
+    ("multipeak8", 8, 256, 3, (2, 400)),         # one full group
+    ("genz_oscillatory6", 6, 100, 3, (2, 50)),   # one partial group
+    ("gaussian", 3, 50, 5, (2, 30)),             # generic (runtime-dims) kernel
+])
+def test_fill_layouts_match_oracle(monkeypatch, layout, chunk, name, dims, ng, ns, nh):
+    # the histogram paths used when d*ng does not fit in shared memory
+    # (hist.cuh records, chunked or not; global atomics), forced on small cases
+    monkeypatch.setenv("VPB_FILL_LAYOUT", layout)
+    if chunk:
+        monkeypatch.setenv("VPB_REC_CHUNK", chunk)
+    test_fill_matches_oracle(name, dims, ng, ns, nh)
+
+
 def test_fill_cube_sums_deterministic():
     g = np.random.default_rng(3)
     off = _random_plan(g, 5, 4, 2, 3000)
