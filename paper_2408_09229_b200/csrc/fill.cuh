@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
                 const uint32_t hi16 = j1 <= j ? (uint32_t)iv[j1 <= j ? j1 : 0] : 0u;
                 wv[q] = lo16 | (hi16 << 16);
               }
-              *reinterpret_cast<uint4 *>(a.rec_iv + ((size_t)g * a.rec_ch + (r0 + rr - rec0)) * 8) =
+              *reinterpret_cast<uint4 *>(
+                  a.rec_iv + ((size_t)g * a.rec_ch + (T0 - rec0) + rr * 32 + lane) * 8) =
                   make_uint4(wv[0], wv[1], wv[2], wv[3]);
             }
           }
@@ -335,11 +336,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           // ---- interval histograms (vp/kernels.py:100-105)
           constexpr bool RT = LAYOUT == LAYOUT_RUNTIME;
           if (LAYOUT == LAYOUT_RECORDS) {
-            a.rec_w2[r0 + rr - rec0] = w2;   // intervals were stored while sampling
+            a.rec_w2[(T0 - rec0) + rr * 32 + lane] = w2;   // intervals stored while sampling
           } else if (RT && a.records) {
             // deferred to hist_records_kernel: w^2 and the intervals, 8 axes
             // per 16-byte group (coalesced over a warp's RPT-strided rows)
-            const long long ri = r0 + rr - rec0;
+            const long long ri = (T0 - rec0) + rr * 32 + lane;   // lane-interleaved slot
             a.rec_w2[ri] = w2;
             constexpr int NG = (MAXD + 7) / 8;
 #pragma unroll

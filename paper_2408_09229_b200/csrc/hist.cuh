@@ -52,18 +52,36 @@ __global__ void __launch_bounds__(HR_NT, 2)
     s_hc[i] = first ? 0u : gc[i];
   }
   __syncthreads();
+  // Record slots are lane-interleaved per fill tile (slot = tile*TILE +
+  // step*32 + lane holds run tile*TILE + lane*RPT + step, so a warp's record
+  // stores are coalesced); the last tile of the shard may have empty slots.
+  const long long nslots = (n + FILL_TILE - 1) / FILL_TILE * FILL_TILE;
   // warp w of CTA b takes span w*B + b of NW*B equal spans: the warps sharing
   // this CTA's histograms sit n/NW records apart (different strata)
   constexpr int NW = HR_NT / 32;
   const long long spans = (long long)NW * gridDim.x;
-  const long long per = (n + spans - 1) / spans;
+  const long long per = ((nslots + spans - 1) / spans + 31) / 32 * 32;
   const long long beg = ((long long)warp * gridDim.x + blockIdx.x) * per;
-  const long long end = min(beg + per, n);
+  const long long end = min(beg + per, nslots);
   const unsigned short *iv_g = rec_iv + (size_t)g * rec_ch * 8;
   const int rot = lane % JN;
-  for (long long i = beg + lane; i < end; i += 32) {
-    const uint4 v = *reinterpret_cast<const uint4 *>(iv_g + (size_t)i * 8);
-    const double w2 = rec_w2[i];
+  auto valid = [&](long long s) {
+    const long long t = s / FILL_TILE, q = s - t * FILL_TILE;
+    return t * FILL_TILE + (q & 31) * FILL_RPT + (q >> 5) < n;
+  };
+  // one record ahead in flight (the loop body is a chain of shared atomics)
+  long long i = beg + lane;
+  uint4 vn = make_uint4(0, 0, 0, 0);
+  double wn = 0.0;
+  if (i < end) { vn = *reinterpret_cast<const uint4 *>(iv_g + (size_t)i * 8); wn = rec_w2[i]; }
+  for (; i < end; i += 32) {
+    const uint4 v = vn;
+    const double w2 = wn;
+    if (i + 32 < end) {
+      vn = *reinterpret_cast<const uint4 *>(iv_g + (size_t)(i + 32) * 8);
+      wn = rec_w2[i + 32];
+    }
+    if (!valid(i)) continue;
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
     int idx[JN];
 #pragma unroll
