@@ -63,7 +63,9 @@ extern "C" {
 #define VPB_ROOS_ARNOLD 9
 #define VPB_MOROKOFF 10         /* [(1+1/d)^d, 1/d]                              */
 #define VPB_CONSTANT 11         /* [c]                                           */
-#define VPB_N_INTEGRANDS 12
+#define VPB_ASIAN_OPTION 12     /* [s0, strike, drift, sigma sqrt(T), exp(-rT), clamp eps] */
+#define VPB_PATH_INTEGRAL 13    /* [m/(2a), a/2, amp, x_end]  (dims = n_slices - 1) */
+#define VPB_N_INTEGRANDS 14
 
 #define VPB_MAX_PARAMS 64
 #define VPB_MAX_DIMS 64

@@ -117,17 +117,34 @@ def sample_runs(seed, batch, run_base, run_start, n, offsets, cube_start, edges,
 ORACLE_IDS = {"gaussian": 0, "ridge": 1, "multipeak8": 2, "genz_oscillatory6": 3,
               "genz_productpeak6": 4, "sinexp": 5, "linear": 6, "cosine": 7,
               "exponential": 8, "roos_arnold": 9, "morokoff": 10, "constant": 11,
-              "gaussian20": 0}
+              "gaussian20": 0, "asian_option": 12, "path_integral": 13}
 
 _DIMS = {"gaussian": 4, "ridge": 4, "multipeak8": 8, "genz_oscillatory6": 6,
          "genz_productpeak6": 6, "sinexp": 2, "linear": 10, "cosine": 10,
-         "exponential": 10, "roos_arnold": 10, "morokoff": 8, "gaussian20": 20}
+         "exponential": 10, "roos_arnold": 10, "morokoff": 8, "gaussian20": 20,
+         "asian_option": 16, "path_integral": 7}
+
+# vp/integrands.py:190, 226-227 (ASIAN_DEFAULTS, PATH_DEFAULTS, CLAMP_EPS)
+ASIAN_DEFAULTS = dict(s0=100.0, strike=100.0, rate=0.05, sigma=0.2, maturity=1.0)
+PATH_DEFAULTS = dict(mass=1.0, total_time=4.0, x_end=0.0)
 
 
-def integrand_params(name: str, dims: int | None = None, value: float = 1.0) -> np.ndarray:
+def integrand_params(name: str, dims: int | None = None, value: float = 1.0,
+                     **kw) -> np.ndarray:
     """Parameter blob for the C evaluator, built with the reference's own
-    Python expressions (vp/integrands.py:131-190, oracle/integrands_np.py)."""
+    Python expressions (vp/integrands.py:131-251, oracle/integrands_np.py)."""
     d = dims or _DIMS.get(name, 1)
+    if name == "asian_option":   # vp/integrands.py:196-210
+        q = dict(ASIAN_DEFAULTS, **kw)
+        drift = (q["rate"] - 0.5 * q["sigma"] * q["sigma"]) * q["maturity"]
+        return np.array([q["s0"], q["strike"], drift, q["sigma"] * math.sqrt(q["maturity"]),
+                         math.exp(-q["rate"] * q["maturity"]), 1e-12])
+    if name == "path_integral":   # vp/integrands.py:233-251, n_slices = d + 1
+        q = dict(PATH_DEFAULTS, **kw)
+        n_slices = d + 1
+        a = q["total_time"] / n_slices
+        amp = (q["mass"] / (2.0 * math.pi * a)) ** (n_slices / 2.0)
+        return np.array([q["mass"] / (2.0 * a), 0.5 * a, amp, q["x_end"]])
     if name in ("gaussian", "gaussian20"):
         mu, sigma = (0.5, 0.01) if name == "gaussian" else (0.5, 0.1)
         norm = (2.0 * math.pi * sigma ** 2) ** (-d / 2.0)

@@ -353,10 +353,32 @@ def gen_integrands():
     x20 = 0.5 + 0.15 * g.standard_normal((4096, 20))
     out["x20"] = x20
     out["gaussian20"] = integrands_np.gaussian20(x20)
+    # reference application integrands (vp/integrands.py:196-251), default
+    # and non-default parameters, straight from the reference
+    x16 = g.random((4096, 16))
+    x16[:4] = [[0.0] * 16, [1.0] * 16, [0.5] * 16, [1e-13] * 16]
+    out["x16"] = x16
+    out["asian_option"] = lookup("asian_option").evaluate_batch(x16)
+    x4a = g.random((4096, 4))
+    out["x4a"] = x4a
+    out["asian_option_k90_d4"] = lookup("asian_option", dim=4, strike=90.0,
+                                        sigma=0.3).evaluate_batch(x4a)
+    x7 = -5.0 + 10.0 * g.random((4096, 7))
+    x7[:1024] *= 0.2          # points near the classical path (non-negligible weights)
+    out["x7"] = x7
+    out["path_integral"] = lookup("path_integral").evaluate_batch(x7)
+    x3 = -5.0 + 10.0 * g.random((4096, 3))
+    x3 *= 0.3
+    out["x3"] = x3
+    out["path_integral_d3_xend05"] = lookup("path_integral", dim=3, x_end=0.5,
+                                            total_time=2.0).evaluate_batch(x3)
     save("integrands.npz", **out)
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["integrands"]:
+        gen_integrands()
+        sys.exit(0)
     gen_philox()
     gen_sample()
     gen_fill()

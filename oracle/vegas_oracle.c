@@ -129,7 +129,44 @@ enum {
   VO_ROOS_ARNOLD = 9,
   VO_MOROKOFF = 10,  /* p = [(1+1/d)^d, 1/d]                                */
   VO_CONSTANT = 11,  /* p = [c]                                             */
+  VO_ASIAN = 12,     /* p = [s0, strike, drift, sigma sqrt(T), exp(-rT), clamp eps] */
+  VO_PATH = 13,      /* p = [m/(2a), 0.5 a, amp, x_end]                     */
 };
+
+/* vp/integrands.py:59-100: Acklam's normal quantile (central + upper tail;
+ * the callers only pass p >= 0.5) refined by one Newton step in erfc space. */
+static const double AK_A[6] = {-3.969683028665376e+01, 2.209460984245205e+02,
+                               -2.759285104469687e+02, 1.383577518672690e+02,
+                               -3.066479806614716e+01, 2.506628277459239e+00};
+static const double AK_B[5] = {-5.447609879822406e+01, 1.615858368580409e+02,
+                               -1.556989798598866e+02, 6.680131188771972e+01,
+                               -1.328068155288572e+01};
+static const double AK_C[6] = {-7.784894002430293e-03, -3.223964580411365e-01,
+                               -2.400758277161838e+00, -2.549732539343734e+00,
+                               4.374664141464968e+00, 2.938163982698783e+00};
+static const double AK_D[4] = {7.784695709041462e-03, 3.224671290700398e-01,
+                               2.445134137142996e+00, 3.754408661907416e+00};
+static double ndtri_approx(double p) {
+  if (p < 0.02425) {
+    double q = sqrt(-2.0 * log(p));
+    return (((((AK_C[0] * q + AK_C[1]) * q + AK_C[2]) * q + AK_C[3]) * q + AK_C[4]) * q + AK_C[5]) /
+           ((((AK_D[0] * q + AK_D[1]) * q + AK_D[2]) * q + AK_D[3]) * q + 1.0);
+  }
+  if (p > 1.0 - 0.02425) {
+    double q = sqrt(-2.0 * log(1.0 - p));
+    return -(((((AK_C[0] * q + AK_C[1]) * q + AK_C[2]) * q + AK_C[3]) * q + AK_C[4]) * q + AK_C[5]) /
+           ((((AK_D[0] * q + AK_D[1]) * q + AK_D[2]) * q + AK_D[3]) * q + 1.0);
+  }
+  double q = p - 0.5, r = q * q;
+  return (((((AK_A[0] * r + AK_A[1]) * r + AK_A[2]) * r + AK_A[3]) * r + AK_A[4]) * r + AK_A[5]) * q /
+         (((((AK_B[0] * r + AK_B[1]) * r + AK_B[2]) * r + AK_B[3]) * r + AK_B[4]) * r + 1.0);
+}
+static double vo_erfinv(double y) {   /* vp/integrands.py:83-100 */
+  double ya = fabs(y);
+  double z = ndtri_approx((ya + 1.0) * 0.5) * (1.0 / sqrt(2.0));
+  z += (erfc(z) - (1.0 - ya)) * (sqrt(M_PI) / 2.0) * exp(z * z);
+  return copysign(z, y);
+}
 
 static int cmp_double(const void *a, const void *b) {
   double x = *(const double *)a, y = *(const double *)b;
@@ -141,7 +178,7 @@ double vo_pairwise_sum(const double *a, int64_t n);
 /* numpy row reductions `.sum(axis=1)` run the pairwise kernel per row (the
  * 8-accumulator path for 8 <= d <= 128); products reduce sequentially. */
 static double eval_one(int id, const double *p, const double *x, int d) {
-  double t[64];
+  double t[66];
   switch (id) {
     case VO_GAUSSIAN: { /* vp/integrands.py:135-139 */
       for (int j = 0; j < d; j++) { double u = x[j] - p[0]; t[j] = u * u; }
@@ -207,6 +244,27 @@ static double eval_one(int id, const double *p, const double *x, int d) {
       double s = 1.0; for (int j = 0; j < d; j++) s *= pow(x[j], p[1]); return p[0] * s;
     }
     case VO_CONSTANT: return p[0];
+    case VO_ASIAN: { /* vp/integrands.py:196-210 asian_option_batch */
+      for (int j = 0; j < d; j++) {
+        double xc = x[j] < p[5] ? p[5] : (x[j] > 1.0 - p[5] ? 1.0 - p[5] : x[j]);
+        t[j] = vo_erfinv(2.0 * xc - 1.0);
+      }
+      double z = vo_pairwise_sum(t, d) * sqrt(2.0);
+      double s_avg = p[0] * exp(p[2] + p[3] * z);
+      double pay = s_avg - p[1];
+      return p[4] * (pay > 0.0 ? pay : 0.0);
+    }
+    case VO_PATH: { /* vp/integrands.py:233-251 path_integral_batch, d = n_slices - 1 */
+      double full[66], kin[65];
+      full[0] = p[3];
+      full[d + 1] = p[3];
+      for (int j = 0; j < d; j++) full[j + 1] = x[j];
+      for (int j = 0; j <= d; j++) { double u = full[j + 1] - full[j]; kin[j] = u * u; }
+      for (int j = 0; j <= d; j++) t[j] = full[j] * full[j];
+      double kinetic = p[0] * vo_pairwise_sum(kin, d + 1);
+      double potential = p[1] * vo_pairwise_sum(t, d + 1);
+      return p[2] * exp(-(kinetic + potential));
+    }
   }
   return NAN;
 }

@@ -1134,7 +1134,7 @@ int vpb_eval_host(int32_t id, const double *params, int32_t n_params, const doub
   const unsigned g = nblk(n, 128);
   switch (id) {
 #define X(I) case I: eval_kernel<I><<<g, 128>>>(dx.p, n, dims, P, o.p); break;
-    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11)
+    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13)
 #undef X
   }
   CK(cudaGetLastError());

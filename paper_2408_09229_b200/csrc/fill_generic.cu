@@ -25,7 +25,7 @@ cudaError_t occ_g(size_t smem, int *ctas) {
 }
 }  // namespace
 
-#define VPB_ALL_IDS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11)
+#define VPB_ALL_IDS(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13)
 
 cudaError_t launch_fill_generic(int id, int grid, size_t smem, cudaStream_t st,
                                 const FillArgs &a) {

@@ -40,7 +40,9 @@ cudaError_t occ_one(size_t smem, int *ctas) {
   X(VPB_COSINE, 10)               \
   X(VPB_EXPONENTIAL, 10)          \
   X(VPB_ROOS_ARNOLD, 10)          \
-  X(VPB_MOROKOFF, 8)
+  X(VPB_MOROKOFF, 8)              \
+  X(VPB_ASIAN_OPTION, 16)         \
+  X(VPB_PATH_INTEGRAL, 7)
 
 int fill_is_specialised(int id, int dims) {
 #define X(I, D) if (id == I && dims == D) return 1;

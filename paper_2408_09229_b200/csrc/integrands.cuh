@@ -35,6 +35,40 @@ __device__ __forceinline__ void cswap(double &a, double &b) {
   a = lo; b = hi;
 }
 
+// ------------------------------------------------------------- erfinv ----
+// vp/integrands.py:59-100: Acklam's rational normal quantile (central region
+// and upper tail -- the Asian payoff only asks for p = (|y|+1)/2 >= 1/2),
+// then one Newton step in erfc space, sign restored by copysign.  Same
+// operation order as the numpy code (unfused); erfc/log/exp are the device
+// libm, so values agree with scipy to a few ulp.
+static __constant__ double kAk[21] = {
+    -3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,    // A
+    1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00,
+    -5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,    // B
+    6.680131188771972e+01, -1.328068155288572e+01,
+    -7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,   // C
+    -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00,
+    7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,      // D
+    3.754408661907416e+00};
+__device__ __forceinline__ double ndtri_upper(double p) {   // p >= 0.5
+  if (p > 1.0 - 0.02425) {
+    const double q = __dsqrt_rn(-2.0 * log(1.0 - p));
+    const double num = (((((kAk[11] * q + kAk[12]) * q + kAk[13]) * q + kAk[14]) * q + kAk[15]) * q + kAk[16]);
+    const double den = ((((kAk[17] * q + kAk[18]) * q + kAk[19]) * q + kAk[20]) * q + 1.0);
+    return __ddiv_rn(-num, den);
+  }
+  const double q = p - 0.5, r = q * q;
+  const double num = (((((kAk[0] * r + kAk[1]) * r + kAk[2]) * r + kAk[3]) * r + kAk[4]) * r + kAk[5]) * q;
+  const double den = (((((kAk[6] * r + kAk[7]) * r + kAk[8]) * r + kAk[9]) * r + kAk[10]) * r + 1.0);
+  return __ddiv_rn(num, den);
+}
+__device__ __forceinline__ double erfinv_ref(double y) {
+  const double ya = fabs(y);
+  double z = ndtri_upper((ya + 1.0) * 0.5) * 0.70710678118654746;   // * (1/sqrt(2))
+  z = z + ((erfc(z) - (1.0 - ya)) * 0.88622692545275801) * fast_exp(z * z);  // sqrt(pi)/2
+  return copysign(z, y);
+}
+
 template <int ID, int D>
 __device__ __forceinline__ double integrand(const double *x, int d, const IParams &P) {
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
@@ -175,6 +209,42 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
       prod = __dmul_rn(prod, pow(x[j], P.p[1]));
     }
     return __dmul_rn(P.p[0], prod);
+  } else if constexpr (ID == VPB_ASIAN_OPTION) {
+    // exp(-rT) max(s0 exp(drift + sigma sqrt(T) z) - K, 0),
+    // z = sqrt(2) sum_i erfinv(2 clip(x_i) - 1)        vp/integrands.py:196-210
+    double t[MAXD];
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D : d); j++) {
+      const double xc = fmin(fmax(x[j], P.p[5]), 1.0 - P.p[5]);
+      t[j] = erfinv_ref(2.0 * xc - 1.0);
+    }
+    const double z = row_sum<D>(t, d) * 1.4142135623730951;   // * math.sqrt(2.0)
+    const double s_avg = P.p[0] * fast_exp(P.p[2] + P.p[3] * z);
+    return P.p[4] * fmax(s_avg - P.p[1], 0.0);
+  } else if constexpr (ID == VPB_PATH_INTEGRAL) {
+    // amp exp(-(m/(2a) sum (x_{j+1}-x_j)^2 + a/2 sum_{j<N} x_j^2)) with fixed
+    // endpoints x_0 = x_N = x_end, N = d + 1          vp/integrands.py:233-251
+    constexpr int MAXN = MAXD + 1;
+    double kin[MAXN], pot[MAXN];
+    const int n = (D > 0 ? D : d) + 1;
+    double prev = P.p[3];
+#pragma unroll
+    for (int j = 0; j < (D > 0 ? D + 1 : n); j++) {
+      const double cur = (j < (D > 0 ? D : d)) ? x[j] : P.p[3];
+      const double u = cur - prev;
+      kin[j] = u * u;
+      pot[j] = prev * prev;
+      prev = cur;
+    }
+    double ks, ps;
+    if constexpr (D > 0) {
+      ks = pw_sum<D + 1>(kin);
+      ps = pw_sum<D + 1>(pot);
+    } else {
+      ks = pw_sum_rt(kin, n);
+      ps = pw_sum_rt(pot, n);
+    }
+    return P.p[2] * fast_exp(-(P.p[0] * ks + P.p[1] * ps));
   } else {
     return P.p[0];   // VPB_CONSTANT
   }

@@ -17,8 +17,11 @@ Registry entries
     genz_productpeak6 cfg4b: prod 1/(a^-2 + (x-u)^2), default_rng(2025), sum a = 7.25
     gaussian20        cfg5: d=20, mu=0.5, sigma=0.1
   plus ``constant`` (value param) for exactness tests.
-The reference's application integrands (asian_option, path_integral) have no
-device functor yet.
+  reference application integrands (vp/integrands.py:186-251, 368-396):
+    asian_option      discounted Asian call payoff on erfinv-transformed uniforms
+                      (dim = number of averaging dates, default 16)
+    path_integral     harmonic-oscillator lattice path-integral weight
+                      (dim = interior points = n_slices - 1, default 7)
 """
 
 from __future__ import annotations
@@ -45,6 +48,15 @@ VPB_EXPONENTIAL = 8
 VPB_ROOS_ARNOLD = 9
 VPB_MOROKOFF = 10
 VPB_CONSTANT = 11
+VPB_ASIAN_OPTION = 12
+VPB_PATH_INTEGRAL = 13
+
+# vp/integrands.py:21, 190-191, 226-227
+CLAMP_EPS = 1e-12
+ASIAN_DEFAULTS = dict(s0=100.0, strike=100.0, rate=0.05, sigma=0.2, maturity=1.0,
+                      n_averages=16)
+PATH_DEFAULTS = dict(mass=1.0, total_time=4.0, n_slices=8, x_end=0.0)
+PATH_BOX_HALF_WIDTH = 5.0
 
 
 class UnknownIntegrandError(VegasError, LookupError):
@@ -187,6 +199,106 @@ def _exp_axis_quad():
     return axis
 
 
+# ------------------------------------------------- application integrands --
+
+def asian_option_reference(s0, strike, rate, sigma, maturity, n_averages):
+    """Closed-form value (vp/integrands.py:213-228): the exponent is normal
+    with effective volatility sigma sqrt(n T), a Black-Scholes expectation."""
+    m = (rate - 0.5 * sigma * sigma) * maturity
+    s = sigma * math.sqrt(maturity * n_averages)
+    if strike <= 0.0:
+        return math.exp(-rate * maturity) * (s0 * math.exp(m + 0.5 * s * s) - strike)
+    d2 = (m + math.log(s0 / strike)) / s
+    d1 = d2 + s
+    phi = lambda t: 0.5 * (1.0 + math.erf(t / math.sqrt(2.0)))
+    return math.exp(-rate * maturity) * (
+        s0 * math.exp(m + 0.5 * s * s) * phi(d1) - strike * phi(d2))
+
+
+def _asian_params(s0, strike, rate, sigma, maturity):
+    # device blob of vp/integrands.py:196-210's constants, same expressions
+    drift = (rate - 0.5 * sigma * sigma) * maturity
+    return [s0, strike, drift, sigma * math.sqrt(maturity), math.exp(-rate * maturity),
+            CLAMP_EPS]
+
+
+def path_integral_lattice_exact(mass, total_time, n_slices, x_end):
+    """Exact lattice integral (vp/integrands.py:254-282): the action is
+    quadratic in the interior points, so it is a Gaussian determinant."""
+    n_int = n_slices - 1
+    a = total_time / n_slices
+    amp = (mass / (2.0 * math.pi * a)) ** (n_slices / 2.0)
+    const = mass / a * x_end ** 2 + 0.5 * a * x_end ** 2
+    if n_int == 0:
+        return amp * math.exp(-const)
+    h = np.zeros((n_int, n_int))
+    np.fill_diagonal(h, 2.0 * mass / a + a)
+    ii = np.arange(n_int - 1)
+    h[ii, ii + 1] = -mass / a
+    h[ii + 1, ii] = -mass / a
+    b = np.zeros(n_int)
+    b[0] -= mass / a * x_end
+    b[-1] -= mass / a * x_end
+    sol = np.linalg.solve(h, b)
+    s_min = const - 0.5 * float(b @ sol)
+    sign, logdet = np.linalg.slogdet(h)
+    assert sign > 0
+    return float(amp * math.exp(-s_min) * (2.0 * math.pi) ** (n_int / 2.0)
+                 * math.exp(-0.5 * logdet))
+
+
+def oscillator_propagator(omega, total_time, x_end, mass=1.0):
+    """Continuum Euclidean propagator <x|e^{-HT}|x> (vp/integrands.py:285-290)."""
+    wt = omega * total_time
+    return math.sqrt(mass * omega / (2.0 * math.pi * math.sinh(wt))) * math.exp(
+        -mass * omega * x_end ** 2 * math.tanh(wt / 2.0))
+
+
+def _path_params(mass, total_time, n_slices, x_end):
+    # vp/integrands.py:233-251: A exp(-(m/(2a) sum dx^2 + a/2 sum x^2))
+    a = total_time / n_slices
+    amp = (mass / (2.0 * math.pi * a)) ** (n_slices / 2.0)
+    return [mass / (2.0 * a), 0.5 * a, amp, x_end]
+
+
+def _spec_asian_option(dim=None, **params):
+    """vp/integrands.py:361-377 (same parameter handling)."""
+    p = dict(ASIAN_DEFAULTS)
+    if dim is not None:
+        p["n_averages"] = int(dim)
+    p.update(params)
+    n = int(p.pop("n_averages"))
+    ref = asian_option_reference(n_averages=n, **p)
+    blob = _asian_params(**p)
+    return _spec("asian_option", n, VPB_ASIAN_OPTION, _fixed(blob), ref, "closed form",
+                 f"params {dict(p, n_averages=n)}")
+
+
+def _spec_path_integral(dim=None, **params):
+    """vp/integrands.py:380-396 (same parameter handling)."""
+    p = dict(PATH_DEFAULTS)
+    if dim is not None:
+        p["n_slices"] = int(dim) + 1
+    p.update(params)
+    n_slices = int(p["n_slices"])
+    dims = n_slices - 1
+    half = float(p.pop("box_half_width", PATH_BOX_HALF_WIDTH))
+    if dims < 1:
+        raise ContractViolationError("path_integral needs at least one interior point")
+    ref = path_integral_lattice_exact(p["mass"], p["total_time"], n_slices, p["x_end"])
+    blob = _path_params(p["mass"], p["total_time"], n_slices, p["x_end"])
+
+    def params_for(d, _blob=blob, _dims=dims):
+        if d != _dims:
+            raise ContractViolationError(
+                f"path_integral: expected {_dims} interior points, got {d}")
+        return _blob
+
+    return _spec("path_integral", dims, VPB_PATH_INTEGRAL, params_for, ref, "oracle",
+                 f"lattice Gaussian determinant; params {p}",
+                 bounds=tuple((-half, half) for _ in range(dims)))
+
+
 # ----------------------------------------------------------------- builders --
 
 def _spec(name, dims, dev_id, param_fn, ref, method, note="", bounds=None):
@@ -225,6 +337,8 @@ _BUILDERS = {
         "genz_productpeak6", 6, VPB_GENZ_PRODUCTPEAK,
         _fixed(list(GENZ_PP_A ** -2.0) + list(GENZ_PP_U)), _genz_pp_reference(),
         "closed form", "BASELINE cfg4b, default_rng(2025), sum a = 7.25"),
+    "asian_option": _spec_asian_option,
+    "path_integral": _spec_path_integral,
     "gaussian20": lambda: _spec("gaussian20", 20, VPB_GAUSSIAN, _gauss_params(0.5, 0.1),
                                 _erf_axis(0.5, 0.1) ** 20, "closed form",
                                 "BASELINE cfg5: d=20, sigma=0.1"),
@@ -253,6 +367,8 @@ def lookup(name: str, dim: int | None = None, **params) -> IntegrandSpec:
         builder = _BUILDERS[name]
     except KeyError:
         raise UnknownIntegrandError(name) from None
+    if name in ("asian_option", "path_integral"):
+        return builder(dim=dim, **params)
     if dim is not None or params:
         raise ValueError(f"integrand {name!r} has fixed dimension and parameters")
     return builder()

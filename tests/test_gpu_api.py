@@ -236,3 +236,53 @@ def test_nccl_path_world1_matches_single():
     assert a.evals_per_iteration == b.evals_per_iteration
     np.testing.assert_allclose([r.estimate for r in a.iterations],
                                [r.estimate for r in b.iterations], rtol=1e-12)
+
+
+# ------------------------------------------------- application integrands --
+# pkg/tests/test_integrands.py:114-262 against the device functors
+
+def test_application_integrands_finite_on_million_points():
+    for name in ("asian_option", "path_integral"):
+        spec = P.lookup(name)
+        lo = np.array([b[0] for b in spec.bounds])
+        hi = np.array([b[1] for b in spec.bounds])
+        pts = lo + (hi - lo) * np.random.default_rng(98).random((1_000_000, spec.dims))
+        assert np.isfinite(spec.evaluate_batch(pts)).all(), name
+
+
+def test_asian_symmetry_point_and_clamping():
+    spec = P.lookup("asian_option")
+    val = spec.evaluate_batch(np.full((1, 16), 0.5))
+    s_avg = 100.0 * math.exp((0.05 - 0.02) * 1.0)
+    assert val[0] == pytest.approx(math.exp(-0.05) * max(s_avg - 100.0, 0.0), rel=1e-12)
+    x = np.zeros((2, 16))
+    x[1] = 1.0
+    assert np.isfinite(spec.evaluate_batch(x)).all()
+    assert P.lookup("asian_option", dim=12).dims == 12
+
+
+def test_asian_option_full_integration_run():
+    spec = P.lookup("asian_option")
+    out = integrate(spec.evaluate_batch, spec.bounds, n_eval=2_000_000, max_it=10, skip=3,
+                    seed=21)
+    assert abs(out.mean - spec.reference_value) < 5 * out.sigma
+    assert out.sigma / spec.reference_value < 0.01
+
+
+def test_path_integral_full_integration_run():
+    spec = P.lookup("path_integral")      # N=8 -> 7 interior dimensions
+    assert spec.dims == 7
+    out = integrate(spec.evaluate_batch, spec.bounds, n_eval=100_000, max_it=10, skip=3,
+                    seed=21, batched=True, workers=2)
+    assert abs(out.mean - spec.reference_value) < 5 * out.sigma
+    assert out.sigma / spec.reference_value < 0.05
+
+
+def test_path_integral_dim_override():
+    from paper_2408_09229_b200.integrands import path_integral_lattice_exact
+    spec = P.lookup("path_integral", dim=4)   # 4 interior points -> N=5
+    assert spec.dims == 4
+    assert spec.reference_value == pytest.approx(
+        path_integral_lattice_exact(1.0, 4.0, 5, 0.0), rel=1e-12)
+    out = integrate(spec.evaluate_batch, spec.bounds, n_eval=200_000, max_it=10, skip=3, seed=4)
+    assert abs(out.mean - spec.reference_value) < 5 * out.sigma

@@ -135,6 +135,20 @@ def test_integrand_values(golden):
         np.testing.assert_allclose(v, g[name], rtol=1e-13, atol=atol, err_msg=name)
 
 
+def test_application_integrand_values(golden):
+    # device erfinv / lattice action vs the reference's own values
+    g = golden("integrands.npz")
+    cases = [(P.lookup("asian_option"), "x16", "asian_option", 2e-11),
+             (P.lookup("asian_option", dim=4, strike=90.0, sigma=0.3), "x4a",
+              "asian_option_k90_d4", 2e-11),
+             (P.lookup("path_integral"), "x7", "path_integral", 1e-300),
+             (P.lookup("path_integral", dim=3, x_end=0.5, total_time=2.0), "x3",
+              "path_integral_d3_xend05", 1e-300)]
+    for spec, xk, key, atol in cases:
+        v = spec.evaluate_batch(g[xk])
+        np.testing.assert_allclose(v, g[key], rtol=1e-12, atol=atol, err_msg=key)
+
+
 def test_registry_reference_integrands_match_oracle():
     g = np.random.default_rng(7)
     for name in ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff"):

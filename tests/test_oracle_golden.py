@@ -131,6 +131,22 @@ def test_integrand_values(golden):
         np.testing.assert_allclose(v, g[name], rtol=2e-13, atol=atol, err_msg=name)
 
 
+def test_application_integrands(golden):
+    # vp/integrands.py:196-251 (asian_option via erfinv, path_integral), default
+    # and non-default parameters, against values from the reference itself.
+    # The payoff max(S - K, 0) cancels near the strike: absolute tolerance.
+    g = golden("integrands.npz")
+    cases = [("asian_option", "x16", {}, "asian_option", 2e-11),
+             ("asian_option", "x4a", dict(strike=90.0, sigma=0.3), "asian_option_k90_d4", 2e-11),
+             ("path_integral", "x7", {}, "path_integral", 1e-300),
+             ("path_integral", "x3", dict(x_end=0.5, total_time=2.0), "path_integral_d3_xend05",
+              1e-300)]
+    for name, xk, kw, key, atol in cases:
+        x = g[xk]
+        v = O.evaluate(name, x, O.integrand_params(name, x.shape[1], **kw))
+        np.testing.assert_allclose(v, g[key], rtol=1e-12, atol=atol, err_msg=key)
+
+
 @pytest.mark.parametrize("traj,name", [("traj_gauss4_small.npz", "gaussian"),
                                        ("traj_ridge_small.npz", "ridge"),
                                        ("traj_genzosc_small.npz", "genz_oscillatory6")])
