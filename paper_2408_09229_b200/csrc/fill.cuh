@@ -387,13 +387,15 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             // f64: the compiler's LDS -> DADD -> ATOMS.CAST.SPIN loop.  (A
             // batched variant -- all d reads, adds and value-returning
             // ATOMS.CAS issued back to back, losers retried -- was measured
-            // 17% slower on cfg2: the value-returning CAS costs more
-            // shared-memory wavefronts than CAST.SPIN and the kernel is
-            // bound by those wavefronts.)
+            // 17% slower on cfg2 at round start and still 8% slower after
+            // the layout changes: the value-returning CAS costs more
+            // shared-memory wavefronts than CAST.SPIN, and wavefronts bind.)
+            {
 #pragma unroll
             for (int j = 0; j < (D > 0 ? D : d); j++) {
               atomicAdd(&s_hw[idx[j]], w2);
               atomicAdd(&s_hc[idx[j]], 1u);
+            }
             }
           } else {
 #pragma unroll
