@@ -173,7 +173,7 @@ struct vpb_ctx {
   double *accf = nullptr;       // [map_w | s1 | s2]
   double *map_w = nullptr, *s1 = nullptr, *s2 = nullptr;
   long long *map_counts = nullptr;
-  double *d_h = nullptr, *dp = nullptr, *pwvals = nullptr;
+  double *d_h = nullptr, *dp = nullptr, *pwvals = nullptr, *pwterms = nullptr;
   PwPlan pw;
   Sched *sched = nullptr;
   Scalars *sc = nullptr;
@@ -194,6 +194,7 @@ struct vpb_ctx {
   int grid = 0;
   bool smem_hist = true;
   bool pairs = false;
+  int hs = 1;                  // shared-histogram row stride
   size_t smem = 0;
   // records mode (histograms too large for shared memory): chunked fill ->
   // hist_records_kernel per 8-axis group
@@ -255,6 +256,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.hc_glob = c->hc_glob;
   a.smem_hist = c->smem_hist ? 1 : 0;
   a.pairs = c->pairs ? 1 : 0;
+  a.hs = c->hs;
   a.records = c->records ? 1 : 0;
   a.tile_lo = 0;
   a.tile_hi = (long long)1 << 62;
@@ -360,10 +362,13 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
 int enqueue_update(vpb_ctx *c, int record) {
   const double V = 1.0 / (double)c->n_cubes;
   const PwPlanDev pd = c->pw.dev();
+  cube_terms_kernel<<<(unsigned)((c->n_cubes + 255) / 256), 256, 0, c->st>>>(
+      c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, c->pwterms, c->status);
   results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
-      c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, pd, c->d_h, c->dp, c->pwvals, c->status);
-  results_tree_kernel<<<1, 1024, 0, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
-                                             c->h_var, c->sched, c->status, record);
+      c->pwterms, c->n_cubes, pd, c->pwvals, c->status);
+  const size_t tsm = pw_tree_smem(pd);
+  results_tree_kernel<<<1, 1024, tsm, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
+                                               c->h_var, c->sched, c->status, record, tsm > 0);
   alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, c->beta,
                                                        (double)c->n_eval, c->uniform_nh, c->sc, 0,
                                                        c->n_h, c->bsum, c->status);
@@ -478,7 +483,7 @@ int upload_uniform_edges(vpb_ctx *c) {
 
 void free_ctx(vpb_ctx *c) {
   void *ptrs[] = {c->edges, c->n_h, c->offsets, c->bsum, c->accf, c->map_counts, c->d_h, c->dp,
-                  c->pwvals, c->sched, c->sc, c->h_est, c->h_var, c->h_evals, c->tile_cube,
+                  c->pwvals, c->pwterms, c->sched, c->sc, c->h_est, c->h_var, c->h_evals, c->tile_cube,
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec};
@@ -595,6 +600,10 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   c->pw.build(nc);
   if ((rc = c->pw.upload()) != VPB_OK) return bail(rc);
   A(c->pwvals, 3 * (size_t)(c->pw.L + c->pw.I));
+  A(c->pwterms, 3 * (size_t)nc);
+  if (cudaFuncSetAttribute(results_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)PW_TREE_SMEM_MAX) != cudaSuccess)
+    return bail(fail(VPB_ERR_CUDA, "results tree smem attribute"));
   A(c->sched, 1);
   A(c->sc, 1);
   A(c->h_est, c->max_it);
@@ -629,14 +638,21 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   c->smem_hist = forced != "records" && forced != "global";
   c->pairs = c->smem_hist && forced != "edges" && fill_is_specialised(c->id, c->dims) &&
              !getenv("VPB_NO_PAIRS");
-  c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1, c->pairs);
-  if (c->pairs && c->smem > (size_t)optin) {
-    c->pairs = false;
-    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 1, 0);
+  // shared-histogram candidates in order: (pairs, padded stride), (pairs,
+  // stride d), (edge rows, padded), (edge rows, stride d)
+  c->hs = hist_stride(c->dims);
+  bool fits = false;
+  for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
+    const bool pr = pass < 2 && c->pairs;
+    if (pass < 2 && !c->pairs) continue;
+    const int hs = (pass & 1) ? c->dims : hist_stride(c->dims);
+    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, pr, hs);
+    if (b <= (size_t)optin) { fits = true; c->pairs = pr; c->hs = hs; c->smem = b; }
   }
-  if (c->smem > (size_t)optin) {
+  if (!fits) {
     c->smem_hist = false;
-    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0);
+    c->pairs = false;
+    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0, 0);
   }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
@@ -657,7 +673,10 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     c->n_groups = (c->dims + 7) / 8;
     const long long cap_runs = c->ntiles_cap * FILL_TILE;
     const long long per_rec = 8 + 16 * (long long)c->n_groups;
-    long long ch = (4ll << 30) / per_rec;   // <= 4 GiB of records per chunk
+    // records per chunk: 1/16 of the iteration's records, within [256 MiB,
+    // 4 GiB] (allocation time at init vs chunk-boundary tails in the fill)
+    const long long want = std::max(256ll << 20, std::min(4ll << 30, cap_runs * per_rec / 16));
+    long long ch = want / per_rec;
     if (const char *e = std::getenv("VPB_REC_CHUNK")) ch = std::max(1ll, std::atoll(e));
     ch -= ch % FILL_TILE;
     if (ch < FILL_TILE) ch = FILL_TILE;
@@ -1268,7 +1287,7 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   pw.build(n);
   TRY(pw.upload());
   struct G { PwPlan *p; ~G() { p->release(); } } g{&pw};
-  DBuf<double> a, b, dh, dp, vals, he, hv;
+  DBuf<double> a, b, dh, dp, vals, he, hv, terms;
   DBuf<long long> doff, hev;
   DBuf<Scalars> sc;
   DBuf<Sched> sch;
@@ -1279,9 +1298,15 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   CK(cudaMemset(st.p, 0, sizeof(int)));
   CK(cudaMemset(sch.p, 0, sizeof(Sched)));
   const double V = 1.0 / (double)n;
-  results_leaf_kernel<<<nblk(8LL * pw.L, 256), 256>>>(a.p, b.p, doff.p, n, V, beta, pw.dev(), dh.p,
-                                                dp.p, vals.p, st.p);
-  results_tree_kernel<<<1, 1024>>>(pw.dev(), vals.p, n, V, sc.p, he.p, hv.p, sch.p, st.p, 0);
+  TRY(terms.alloc(3 * (size_t)n));
+  cube_terms_kernel<<<nblk(n, 256), 256>>>(a.p, b.p, doff.p, n, V, beta, dh.p, dp.p, terms.p,
+                                           st.p);
+  results_leaf_kernel<<<nblk(8LL * pw.L, 256), 256>>>(terms.p, n, pw.dev(), vals.p, st.p);
+  const size_t tsm = pw_tree_smem(pw.dev());
+  CK(cudaFuncSetAttribute(results_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)PW_TREE_SMEM_MAX));
+  results_tree_kernel<<<1, 1024, tsm>>>(pw.dev(), vals.p, n, V, sc.p, he.p, hv.p, sch.p, st.p, 0,
+                                        tsm > 0);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   Scalars s;

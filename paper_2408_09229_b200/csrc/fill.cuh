@@ -88,6 +88,7 @@ struct FillArgs {
   double *rec_w2;               // [rec_ch]
   long long rec_ch;             // records per chunk (a multiple of FILL_TILE)
   int pairs;                    // 1: (E[i], dx[i]) pair table instead of the edge rows
+  int hs;                       // row stride of the shared histograms [interval][axis]
   int *status;                  // bit0 non-finite, bit1 assert
   unsigned long long *err_run;  // min run index with a non-finite value
   IParams P;
@@ -105,6 +106,8 @@ struct SegItem {   // a partial cube segment (key < 0: none)
 // fast index their 8-byte (4-byte) words then fall into distinct bank groups
 // except for lanes sharing an axis, which collide with probability
 // 1/(banks per row) -- instead of random interval addresses colliding freely.
+// The host falls back to the unpadded stride d when the padded rows do not
+// fit (e.g. d = 10 at ng = 1024), before giving up on shared histograms.
 __host__ __device__ inline int hist_stride(int dims) {
   int s = 1;
   while (s < dims) s <<= 1;
@@ -113,11 +116,11 @@ __host__ __device__ inline int hist_stride(int dims) {
 
 // shared-memory layout helper (bytes)
 __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
-                                                  int smem_hist, int pairs) {
+                                                  int smem_hist, int pairs, int hs) {
   size_t b = 0;
   if (pairs) b += (size_t)dims * ng * 2 * sizeof(double);              // (E[i], dx[i])
   else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
-  if (smem_hist) b += (size_t)hist_stride(dims) * ng * (sizeof(double) + sizeof(unsigned));
+  if (smem_hist) b += (size_t)hs * ng * (sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
   b += 16;                                                              // block flags
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   const int d = D > 0 ? D : a.dims;
   const int ng = a.ng;
   const int tid = threadIdx.x;
-  const int hs = D > 0 ? hist_stride(D) : hist_stride(a.dims);   // histogram row stride
+  const int hs = a.hs;   // histogram row stride (hist_stride(d), or d when that does not fit)
 
   // ---- shared memory carve-up
   double *s_edges = reinterpret_cast<double *>(smem_raw);

@@ -62,24 +62,36 @@ __device__ __forceinline__ void cube_terms(const double *s1, const double *s2,
   }
 }
 
-__global__ void results_leaf_kernel(const double *s1, const double *s2, const long long *offsets,
-                                    long long n, double V, double beta, PwPlanDev pw,
-                                    double *d_h, double *dp, double *vals, const int *status) {
+// One thread per cube: the per-cube terms m, rv/c, dp into terms[0|n|2n]
+// (and d_h, dp for the next allocation).  Fully parallel, so the divisions,
+// sqrt and pow do not serialise inside the leaf sums below.
+__global__ void cube_terms_kernel(const double *s1, const double *s2, const long long *offsets,
+                                  long long n, double V, double beta, double *d_h, double *dp,
+                                  double *terms, const int *status) {
+  const long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n || (*status & 1)) return;
+  double m, t, p;
+  cube_terms(s1, s2, offsets, h, V, beta, beta != 0.0, d_h, dp, m, t, p);
+  terms[h] = m;
+  terms[n + h] = t;
+  terms[2 * n + h] = p;
+}
+
+__global__ void results_leaf_kernel(const double *terms, long long n, PwPlanDev pw, double *vals,
+                                    const int *status) {
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int leaf = (int)(gt >> 3), j = (int)(gt & 7);
   if (*status & 1) return;
   const bool live = leaf < pw.L;
   const long long o = live ? pw.leaf_off[leaf] : 0;
   const int len = live ? pw.leaf_len[leaf] : 0;
-  const bool want_dp = beta != 0.0;
+  const double *tm = terms, *tt = terms + n, *tp = terms + 2 * n;
   double rm = 0.0, rt = 0.0, rp = 0.0;
   const int full = len < 8 ? 0 : len - (len % 8);
   if (live && len >= 8) {
-    cube_terms(s1, s2, offsets, o + j, V, beta, want_dp, d_h, dp, rm, rt, rp);
+    rm = tm[o + j]; rt = tt[o + j]; rp = tp[o + j];
     for (int i = 8 + j; i < full; i += 8) {
-      double m, t, p;
-      cube_terms(s1, s2, offsets, o + i, V, beta, want_dp, d_h, dp, m, t, p);
-      rm = __dadd_rn(rm, m); rt = __dadd_rn(rt, t); rp = __dadd_rn(rp, p);
+      rm = __dadd_rn(rm, tm[o + i]); rt = __dadd_rn(rt, tt[o + i]); rp = __dadd_rn(rp, tp[o + i]);
     }
   }
 #pragma unroll
@@ -92,9 +104,7 @@ __global__ void results_leaf_kernel(const double *s1, const double *s2, const lo
   if (!live || j != 0) return;
   if (len < 8) { rm = 0.0; rt = 0.0; rp = 0.0; }
   for (int i = full; i < len; i++) {   // numpy's sequential tail (or n < 8)
-    double m, t, p;
-    cube_terms(s1, s2, offsets, o + i, V, beta, want_dp, d_h, dp, m, t, p);
-    rm = __dadd_rn(rm, m); rt = __dadd_rn(rt, t); rp = __dadd_rn(rp, p);
+    rm = __dadd_rn(rm, tm[o + i]); rt = __dadd_rn(rt, tt[o + i]); rp = __dadd_rn(rp, tp[o + i]);
   }
   vals[3 * leaf + 0] = rm;
   vals[3 * leaf + 1] = rt;
@@ -111,15 +121,35 @@ __global__ void array_leaf_kernel(const double *a, PwPlanDev pw, double *vals) {
 }
 
 // Inner nodes of the pairwise tree, by height, one CTA; three sums at once.
-__device__ void pw_tree_combine(PwPlanDev pw, double *vals) {
+// When the whole tree fits (`sv` != nullptr: dynamic shared memory of
+// 3*(L+I) doubles) the leaves are staged there and every level combines in
+// shared memory; otherwise the levels combine in `vals` (global).
+__device__ void pw_tree_combine(PwPlanDev pw, double *vals, double *sv = nullptr) {
+  double *v = vals;
+  if (sv) {
+    for (int i = threadIdx.x; i < 3 * pw.L; i += blockDim.x) sv[i] = vals[i];
+    __syncthreads();
+    v = sv;
+  }
   for (int h = 0; h < pw.H; h++) {
     for (int i = pw.level_start[h] + threadIdx.x; i < pw.level_start[h + 1]; i += blockDim.x) {
       const int l = pw.node_l[i], r = pw.node_r[i], me = pw.L + i;
 #pragma unroll
-      for (int c = 0; c < 3; c++) vals[3 * me + c] = __dadd_rn(vals[3 * l + c], vals[3 * r + c]);
+      for (int c = 0; c < 3; c++) v[3 * me + c] = __dadd_rn(v[3 * l + c], v[3 * r + c]);
     }
     __syncthreads();
   }
+  if (sv && threadIdx.x < 3) {   // the root, for the caller
+    const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
+    vals[3 * root + threadIdx.x] = sv[3 * root + threadIdx.x];
+  }
+  __syncthreads();
+}
+
+constexpr size_t PW_TREE_SMEM_MAX = 200 * 1024;
+inline size_t pw_tree_smem(const PwPlanDev &pw) {
+  const size_t b = sizeof(double) * 3 * (size_t)(pw.L + pw.I);
+  return b <= PW_TREE_SMEM_MAX ? b : 0;
 }
 
 struct Scalars {
@@ -130,9 +160,10 @@ struct Scalars {
 // Finishes compute_results (vp/strat.py:205-207) and records the history.
 __global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, double V,
                                     Scalars *sc, double *hist_est, double *hist_var,
-                                    Sched *sched, const int *status, int record) {
+                                    Sched *sched, const int *status, int record, int use_smem) {
+  extern __shared__ __align__(16) double tree_sm[];
   if (*status & 1) return;
-  pw_tree_combine(pw, vals);
+  pw_tree_combine(pw, vals, use_smem ? tree_sm : nullptr);
   if (threadIdx.x == 0) {
     const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
     const double sm = vals[3 * root], st = vals[3 * root + 1], sp = vals[3 * root + 2];
@@ -287,33 +318,94 @@ __global__ void set_iteration_kernel(Sched *sched, int it) { sched->it = it; }
 
 // ----------------------------------------------------------------- fill ----
 // Cube chains spanning tiles, in tile order (deterministic).
+// A chain = a root tile whose tail cube starts inside it, the following
+// "through" tiles lying entirely inside that cube, and the tile whose head
+// closes it.  Short chains (no through tile) are closed by the root's own
+// thread; long ones (cubes of many thousand runs: the peaks of an adapted
+// allocation) by the whole warp, 256 tiles per step (8 per lane, loads in
+// flight together): a ballot finds where the chain ends and the through
+// values are summed per lane in tile order, then by a fixed xor butterfly,
+// so the result is deterministic (the order differs from a left fold,
+// within the cube-sum tolerance).
 __global__ void fill_fixup_kernel(FillArgs a) {
   const long long nt = a.sched->ntiles;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  const long long key = a.ck_tail[t];
-  if (t == 0 && a.ck_head[0] >= 0) {   // cube begun before this shard
+  const int lane = threadIdx.x & 31;
+  const bool in = t < nt;
+  if (in && t == 0 && a.ck_head[0] >= 0) {   // cube begun before this shard
     a.s1[a.ck_head[0]] = a.cv_head[0];
     a.s2[a.ck_head[0]] = a.cv_head[1];
   }
-  if (key < 0) return;
-  if (a.ct_through[t] && t != 0) return;   // continuation, owned by an earlier tile
-  double v1 = a.cv_tail[2 * t], v2 = a.cv_tail[2 * t + 1];
-  long long u = t + 1;
-  for (; u < nt; u++) {
-    if (a.ck_tail[u] == key && a.ct_through[u]) {
-      v1 = __dadd_rn(v1, a.cv_tail[2 * u]);
-      v2 = __dadd_rn(v2, a.cv_tail[2 * u + 1]);
-      continue;
+  const long long key = in ? a.ck_tail[t] : -1;
+  const bool root = key >= 0 && (!a.ct_through[t] || t == 0);
+  double v1 = 0.0, v2 = 0.0;
+  bool longc = false;
+  if (root) {
+    v1 = a.cv_tail[2 * t];
+    v2 = a.cv_tail[2 * t + 1];
+    const long long u = t + 1;
+    if (u < nt && a.ck_tail[u] == key && a.ct_through[u]) {
+      longc = true;
+    } else {
+      if (u < nt && a.ck_head[u] == key) {
+        v1 = __dadd_rn(v1, a.cv_head[2 * u]);
+        v2 = __dadd_rn(v2, a.cv_head[2 * u + 1]);
+      }
+      a.s1[key] = v1;
+      a.s2[key] = v2;
     }
-    if (a.ck_head[u] == key) {
-      v1 = __dadd_rn(v1, a.cv_head[2 * u]);
-      v2 = __dadd_rn(v2, a.cv_head[2 * u + 1]);
-    }
-    break;
   }
-  a.s1[key] = v1;
-  a.s2[key] = v2;
+  unsigned todo = __ballot_sync(0xffffffffu, longc);
+  while (todo) {
+    const int leader = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const long long K = __shfl_sync(0xffffffffu, key, leader);
+    const long long T = __shfl_sync(0xffffffffu, t, leader);
+    double acc1 = __shfl_sync(0xffffffffu, v1, leader);
+    double acc2 = __shfl_sync(0xffffffffu, v2, leader);
+    constexpr int PER = 8;   // tiles per lane per step: 256 tiles per warp step
+    for (long long base = T + 1;; base += 32 * PER) {
+      const long long u0 = base + (long long)lane * PER;
+      bool cont[PER];
+      double q1[PER], q2[PER];
+#pragma unroll
+      for (int k = 0; k < PER; k++) {   // independent loads, issued together
+        const long long u = u0 + k;
+        cont[k] = u < nt && a.ck_tail[u] == K && a.ct_through[u];
+        q1[k] = cont[k] ? a.cv_tail[2 * u] : 0.0;
+        q2[k] = cont[k] ? a.cv_tail[2 * u + 1] : 0.0;
+      }
+      int brk = PER;   // this lane's first non-through tile
+#pragma unroll
+      for (int k = PER - 1; k >= 0; k--) if (!cont[k]) brk = k;
+      double p1 = 0.0, p2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < PER; k++)
+        if (k < brk) { p1 = __dadd_rn(p1, q1[k]); p2 = __dadd_rn(p2, q2[k]); }
+      const unsigned bm = __ballot_sync(0xffffffffu, brk < PER);
+      const int first = bm ? __ffs(bm) - 1 : 32;   // lane holding the chain's end
+      if (lane > first) { p1 = 0.0; p2 = 0.0; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p1 = __dadd_rn(p1, __shfl_xor_sync(0xffffffffu, p1, o));
+        p2 = __dadd_rn(p2, __shfl_xor_sync(0xffffffffu, p2, o));
+      }
+      acc1 = __dadd_rn(acc1, p1);
+      acc2 = __dadd_rn(acc2, p2);
+      if (first < 32) {
+        const long long c = base + (long long)first * PER + __shfl_sync(0xffffffffu, brk, first);
+        if (c < nt && a.ck_head[c] == K) {   // the closing tile
+          acc1 = __dadd_rn(acc1, a.cv_head[2 * c]);
+          acc2 = __dadd_rn(acc2, a.cv_head[2 * c + 1]);
+        }
+        break;
+      }
+    }
+    if (lane == leader) {
+      a.s1[K] = acc1;
+      a.s2[K] = acc2;
+    }
+  }
 }
 
 // Sum the per-CTA histogram slices in CTA order (deterministic): block
@@ -329,11 +421,25 @@ __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_par
   const int b0 = p * per, b1 = min(nparts, b0 + per);
   double w = 0.0;
   long long c = 0;
-  if (i < m)
-    for (int b = b0; b < b1; b++) {
+  if (i < m) {
+    // loads issued ahead in groups of 8; the adds stay in slice order
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      double wv[8];
+      unsigned cv[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        wv[k] = hw_part[(size_t)(b + k) * m + i];
+        cv[k] = hc_part[(size_t)(b + k) * m + i];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) { w = __dadd_rn(w, wv[k]); c += cv[k]; }
+    }
+    for (; b < b1; b++) {
       w = __dadd_rn(w, hw_part[(size_t)b * m + i]);
       c += hc_part[(size_t)b * m + i];
     }
+  }
   sw[p][threadIdx.x] = w;
   sc[p][threadIdx.x] = c;
   __syncthreads();
@@ -427,7 +533,7 @@ __device__ double block_pairwise(const double *a, int n, BlockPw &S) {
 // update_grid (vp/maps.py:202-234) on a shared-memory copy of the row.
 // numpy's pairwise sums run block-wide (block_pairwise); the cumsum is
 // inherently sequential (numpy's rounding) and runs on one thread.
-constexpr int REFINE_NT = 256;
+constexpr int REFINE_NT = 1024;
 constexpr int REFINE_SMEM_NG = 2048;   // rows up to this length live in smem
 
 __global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const double *map_w,
