@@ -58,7 +58,6 @@ CONFIGS = {
 }
 METRIC = "integrand evals/sec per iteration (1/2/4/8 B200) + % FP64 roofline vs host CPU ref"
 UNIT = "evals/s"
-FIX_LAUNCHES_PER_ITER = 11   # our kernels per iteration (see capi.cu enqueue_iteration)
 
 
 def fp64_ops_per_eval(cfg) -> float:
@@ -259,6 +258,7 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
     d2h = pinned_out.nbytes + 8 + 8 + 8
     e_integ.close()
 
+    layout = integ.fill_layout()
     if rank == 0:
         ops = fp64_ops_per_eval(cfg)
         # fill kernel: per-rank evaluations = its shard of each plan
@@ -289,7 +289,8 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
                        "n_eval_per_iteration": n_eval, "n_strat": integ.n_strat,
                        "n_cubes": integ.n_cubes, "evals_per_step": evals_timed / steps,
                        "parallelism": f"runs sharded over {world} GPU(s), NCCL all-reduce",
-                       "l2": "flushed (256 MiB write) before every timed iteration"},
+                       "l2": "flushed (256 MiB write) before every timed iteration",
+                       "fill_layout": layout["layout"], "record_chunks": layout["chunks"]},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
                          "peak": peak_ops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_ops, "traffic": traffic,
@@ -301,7 +302,7 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": FIX_LAUNCHES_PER_ITER * steps,
+            "gpu_launches": layout["launches_per_iteration"] * steps,
             "clocks": clocks.summary(),
             "estimates": {"last": float(est[-1]), "sigma_last": float(np.sqrt(var[-1]))},
         }

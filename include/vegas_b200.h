@@ -141,6 +141,12 @@ int vpb_sync(vpb_ctx *ctx);
  * context's stream). */
 int vpb_timing(vpb_ctx *ctx, int32_t first, int32_t count, double *iter_ms,
                double *fill_kernel_ms);
+/* The context's fill layout: 0 edge rows + shared histograms, 1 pair table +
+ * shared histograms, 2 records (chunked fill + hist_records groups), 3
+ * generic runtime-dims kernel; record chunks per iteration (0 if none); and
+ * the number of this library's kernel launches per iteration. */
+int vpb_fill_layout(vpb_ctx *ctx, int32_t *layout, int32_t *n_chunks,
+                    int32_t *launches_per_iteration);
 /* Measured FP64 pipe throughput (DFMA chains on every SM; one FMA = 1 op):
  * the roofline denominator for the FP64-issue-bound fill. */
 int vpb_fp64_peak(int32_t device, double *ops_per_s);

@@ -74,6 +74,7 @@ SIGNATURES = {
     "vpb_sync": [_P],
     "vpb_timing": [_P, _I32, _I32, _c.POINTER(_F64), _c.POINTER(_F64)],
     "vpb_fp64_peak": [_I32, _c.POINTER(_F64)],
+    "vpb_fill_layout": [_P, _c.POINTER(_I32), _c.POINTER(_I32), _c.POINTER(_I32)],
     "vpb_set_edges": [_P, _P],
     "vpb_get_edges": [_P, _P],
     "vpb_set_allocation": [_P, _P],

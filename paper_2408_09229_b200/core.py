@@ -315,6 +315,18 @@ class Integrator:
                                      ctypes.byref(k)))
         return a.value, k.value
 
+    _LAYOUTS = {0: "edge rows + shared histograms", 1: "pair table + shared histograms",
+                2: "records + per-group shared histograms", 3: "generic runtime-dims kernel"}
+
+    def fill_layout(self) -> dict:
+        """The fill's shared-memory layout, record chunks per iteration and
+        this library's kernel launches per iteration (vpb_fill_layout)."""
+        lay, ch, ln = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        N.check(self._lib.vpb_fill_layout(self._ctx, ctypes.byref(lay), ctypes.byref(ch),
+                                          ctypes.byref(ln)))
+        return {"layout": self._LAYOUTS.get(lay.value, str(lay.value)), "chunks": ch.value,
+                "launches_per_iteration": ln.value}
+
     def last_fill_ms(self) -> float:
         t = ctypes.c_double()
         N.check(self._lib.vpb_last_fill_ms(self._ctx, ctypes.byref(t)))

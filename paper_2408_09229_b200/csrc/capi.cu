@@ -195,6 +195,7 @@ struct vpb_ctx {
   bool smem_hist = true;
   bool pairs = false;
   int hs = 1;                  // shared-histogram row stride
+  int layout = 0;              // LAYOUT_* of the fill kernel
   size_t smem = 0;
   // records mode (histograms too large for shared memory): chunked fill ->
   // hist_records_kernel per 8-axis group
@@ -665,6 +666,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
                      : c->pairs               ? LAYOUT_PAIRS
                      : (c->smem_hist && spec) ? LAYOUT_EDGES
                                               : LAYOUT_RUNTIME;
+  c->layout = layout;
   int per_sm = 0;
   if (fill_occupancy(c->id, c->dims, layout, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
     return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
@@ -898,6 +900,17 @@ __global__ void fp64_peak_kernel(double *out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
 }
 }  // namespace
+
+int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *launches) {
+  if (!c) return fail(VPB_ERR_INVALID, "null context");
+  if (layout) *layout = c->layout;
+  if (n_chunks) *n_chunks = c->records ? c->n_chunks : 0;
+  // plan_scan, plan_offsets, fill | chunks x (fill + groups), fixup, histogram
+  // reduce, cube_terms, results_leaf, results_tree, alloc, refine, step, mark
+  const int fill = c->records ? c->n_chunks * (1 + c->n_groups) : 1;
+  if (launches) *launches = 2 + fill + 2 + 3 + 1 + 1 + 2;
+  return VPB_OK;
+}
 
 int vpb_fp64_peak(int32_t device, double *ops_per_s) {
   if (device >= 0) CK(cudaSetDevice(device));
