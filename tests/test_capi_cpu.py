@@ -97,6 +97,16 @@ def test_division_proofs(tmp_path, src):
     assert " 0 mismatches" in r.stdout
 
 
+def test_device_exp_accuracy(tmp_path):
+    # devmath.cuh fast_exp_core restated in C with the same coefficients:
+    # < 1 ulp against expl (tools/proofs/exp_accuracy.c)
+    exe = str(tmp_path / "expacc")
+    subprocess.run(["gcc", "-O2", "-mfma", "-o", exe,
+                    os.path.join(ROOT, "tools", "proofs", "exp_accuracy.c"), "-lm"], check=True)
+    r = subprocess.run([exe, "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_partition_runs_matches_reference_rule():
     from paper_2408_09229_b200.distributed import partition_runs
     assert partition_runs(10, 3) == [(0, 4), (4, 7), (7, 10)]
