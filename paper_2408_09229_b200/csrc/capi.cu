@@ -18,6 +18,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -145,9 +148,72 @@ struct PwPlan {
   }
 };
 
+// Process-wide cache of context buffers.  integrate() creates and destroys a
+// context per call (vp/core.py semantics); reusing device blocks of earlier
+// contexts keeps the init/clear phases at microseconds instead of a
+// cudaMalloc/cudaFree of up to gigabytes per call.  Blocks are keyed by
+// device and size class; a context's stream is synchronised before its
+// blocks return to the cache (vpb_destroy).
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void *> free_blocks;   // (device, bytes) -> ptr
+  std::unordered_map<void *, std::pair<int, size_t>> sizes;
+};
+BlockCache &block_cache() {
+  static BlockCache *c = new BlockCache();   // never destroyed (exit-time order)
+  return *c;
+}
+size_t size_class(size_t b) {
+  const size_t g = b >= (1u << 20) ? (2u << 20) : 512;
+  return (b + g - 1) / g * g;
+}
+cudaError_t cached_malloc(void **p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t want = size_class(bytes);
+  BlockCache &C = block_cache();
+  {
+    std::lock_guard<std::mutex> g(C.mu);
+    auto it = C.free_blocks.lower_bound({dev, want});
+    if (it != C.free_blocks.end() && it->first.first == dev && it->first.second <= 2 * want) {
+      *p = it->second;
+      C.free_blocks.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, want);
+  if (e == cudaErrorMemoryAllocation) {   // give this device's cached blocks back and retry
+    cudaGetLastError();
+    std::lock_guard<std::mutex> g(C.mu);
+    for (auto it = C.free_blocks.begin(); it != C.free_blocks.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        C.sizes.erase(it->second);
+        it = C.free_blocks.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    e = cudaMalloc(p, want);
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(C.mu);
+    C.sizes[*p] = {dev, want};
+  }
+  return e;
+}
+void cached_free(void *p) {
+  if (!p) return;
+  BlockCache &C = block_cache();
+  std::lock_guard<std::mutex> g(C.mu);
+  auto it = C.sizes.find(p);
+  if (it == C.sizes.end()) { cudaFree(p); return; }
+  C.free_blocks.insert({it->second, p});
+}
+
 template <class T>
 int dalloc(T **p, size_t n) {
-  CK(cudaMalloc((void **)p, sizeof(T) * std::max<size_t>(n, 1)));
+  CK(cached_malloc((void **)p, sizeof(T) * std::max<size_t>(n, 1)));
   return VPB_OK;
 }
 
@@ -488,8 +554,7 @@ void free_ctx(vpb_ctx *c) {
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec};
-  for (void *p : ptrs)
-    if (p) cudaFree(p);
+  for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
     for (auto e : E)
@@ -842,7 +907,7 @@ int vpb_error_info(vpb_ctx *c, int64_t *run_index, double *point, double *value)
   CK(cudaStreamSynchronize(c->st));
   std::vector<double> hx(c->dims);
   CK(cudaMemcpy(hx.data(), x, sizeof(double) * c->dims, cudaMemcpyDeviceToHost));
-  cudaFree(jac); cudaFree(idx); cudaFree(cube); cudaFree(f); cudaFree(x);
+  cached_free(jac); cached_free(idx); cached_free(cube); cached_free(f); cached_free(x);
   double v = 0.0;
   std::vector<double> pp(c->P.p, c->P.p + c->P.n);
   TRY(vpb_eval_host(c->id, pp.data(), c->P.n, hx.data(), 1, c->dims, &v));
