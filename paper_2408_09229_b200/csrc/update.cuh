@@ -320,8 +320,8 @@ __global__ void set_iteration_kernel(Sched *sched, int it) { sched->it = it; }
 // Cube chains spanning tiles, in tile order (deterministic).
 // A chain = a root tile whose tail cube starts inside it, the following
 // "through" tiles lying entirely inside that cube, and the tile whose head
-// closes it.  Short chains (no through tile) are closed by the root's own
-// thread; long ones (cubes of many thousand runs: the peaks of an adapted
+// closes it.  Chains with up to 8 through tiles are closed by the root's own
+// thread (tile order); longer ones continue (cubes of many thousand runs: the peaks of an adapted
 // allocation) by the whole warp, 256 tiles per step (8 per lane, loads in
 // flight together): a ballot finds where the chain ends and the through
 // values are summed per lane in tile order, then by a fixed xor butterfly,
@@ -340,17 +340,26 @@ __global__ void fill_fixup_kernel(FillArgs a) {
   const bool root = key >= 0 && (!a.ct_through[t] || t == 0);
   double v1 = 0.0, v2 = 0.0;
   bool longc = false;
+  long long next = t + 1;   // first tile not yet summed
   if (root) {
+    constexpr int SHORT = 8;   // through tiles a lane walks on its own
     v1 = a.cv_tail[2 * t];
     v2 = a.cv_tail[2 * t + 1];
-    const long long u = t + 1;
-    if (u < nt && a.ck_tail[u] == key && a.ct_through[u]) {
-      longc = true;
-    } else {
-      if (u < nt && a.ck_head[u] == key) {
-        v1 = __dadd_rn(v1, a.cv_head[2 * u]);
-        v2 = __dadd_rn(v2, a.cv_head[2 * u + 1]);
+    bool done = false;
+    for (int k = 0; k <= SHORT && !done; k++, next++) {
+      if (next < nt && a.ck_tail[next] == key && a.ct_through[next]) {
+        if (k == SHORT) { longc = true; break; }
+        v1 = __dadd_rn(v1, a.cv_tail[2 * next]);
+        v2 = __dadd_rn(v2, a.cv_tail[2 * next + 1]);
+        continue;
       }
+      if (next < nt && a.ck_head[next] == key) {
+        v1 = __dadd_rn(v1, a.cv_head[2 * next]);
+        v2 = __dadd_rn(v2, a.cv_head[2 * next + 1]);
+      }
+      done = true;
+    }
+    if (done) {
       a.s1[key] = v1;
       a.s2[key] = v2;
     }
@@ -360,11 +369,11 @@ __global__ void fill_fixup_kernel(FillArgs a) {
     const int leader = __ffs(todo) - 1;
     todo &= todo - 1;
     const long long K = __shfl_sync(0xffffffffu, key, leader);
-    const long long T = __shfl_sync(0xffffffffu, t, leader);
+    const long long T = __shfl_sync(0xffffffffu, next, leader);
     double acc1 = __shfl_sync(0xffffffffu, v1, leader);
     double acc2 = __shfl_sync(0xffffffffu, v2, leader);
     constexpr int PER = 8;   // tiles per lane per step: 256 tiles per warp step
-    for (long long base = T + 1;; base += 32 * PER) {
+    for (long long base = T;; base += 32 * PER) {
       const long long u0 = base + (long long)lane * PER;
       bool cont[PER];
       double q1[PER], q2[PER];

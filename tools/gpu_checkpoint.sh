@@ -12,3 +12,5 @@ for c in cfg1 cfg3 cfg4a cfg4b cfg5; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err; echo "bench $c rc=$?"
 done
 bash tools/gpu_profile.sh cfg2 $TAG/p
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 2 -c 1 \
+  -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 4 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
