@@ -807,16 +807,14 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
   TRY(setdev(c));
   ncclUniqueId uid;
   std::memcpy(&uid, id, 128);
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
-  if (c->graph) cudaGraphDestroy(c->graph);
-  if (c->cap_st) cudaStreamDestroy(c->cap_st);
-  if (c->comm) ncclCommDestroy(c->comm);
-  c->comm = nullptr;
+  CK(cudaStreamSynchronize(c->st));
+  // the captured iteration graph embeds the old shard / communicator
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
   NK(ncclCommInitRank(&c->comm, world, uid, rank));
   c->world = world;
   c->rank = rank;
-  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
-  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   return VPB_OK;
 }
 

@@ -18,7 +18,10 @@
 
 namespace vpb {
 
-constexpr int HR_NT = 512;   // threads per CTA (two CTAs per SM)
+#ifndef VPB_HR_NT
+#define VPB_HR_NT 512
+#endif
+constexpr int HR_NT = VPB_HR_NT;   // threads per CTA (two CTAs per SM)
 
 __host__ __device__ inline size_t hist_records_smem(int ng) {
   return (size_t)ng * 8 * (sizeof(double) + sizeof(unsigned));
