@@ -267,6 +267,7 @@ struct vpb_ctx {
   // hist_records_kernel per 8-axis group
   bool records = false;
   long long rec_ch = 0;        // runs per chunk (multiple of FILL_TILE)
+  int rec_k0 = 0;              // leading axes the records-layout fill keeps in shared memory
   int n_chunks = 0, n_groups = 0, rec_B = 0;
   unsigned short *rec_iv = nullptr;
   double *rec_w2 = nullptr, *hw_rec = nullptr;
@@ -321,7 +322,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.hc_part = c->hc_part;
   a.hw_glob = c->hw_glob;
   a.hc_glob = c->hc_glob;
-  a.smem_hist = c->smem_hist ? 1 : 0;
+  a.smem_hist = (c->smem_hist || c->rec_k0 > 0) ? 1 : 0;
   a.pairs = c->pairs ? 1 : 0;
   a.hs = c->hs;
   a.records = c->records ? 1 : 0;
@@ -382,7 +383,7 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
       a.tile_hi = (ch + 1) * tpc;
       CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
       for (int g = 0; g < c->n_groups; g++) {
-        const int jn = std::min(8, c->dims - 8 * g);
+        const int jn = std::min(8, c->dims - c->rec_k0 - 8 * g);
         const size_t goff = (size_t)g * c->rec_B * c->ng * 8;
         const size_t sm = hist_records_smem(c->ng);
 #define VPB_HR(J)                                                                           \
@@ -404,8 +405,13 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   const long long nt = c->ntiles_cap;
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
   if (c->records) {
-    rec_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
-        c->hw_rec, c->hc_rec, c->rec_B, c->dims, c->ng, c->map_w, c->map_counts, c->status);
+    const size_t m0 = (size_t)c->rec_k0 * c->ng;   // rows histogrammed by the fill itself
+    if (m0 > 0)
+      hist_reduce_kernel<<<(unsigned)((m0 + 31) / 32), dim3(32, 8), 0, c->st>>>(
+          c->hw_part, c->hc_part, c->grid, (long long)m0, c->map_w, c->map_counts);
+    rec_reduce_kernel<<<(unsigned)((m - m0 + 31) / 32), dim3(32, 8), 0, c->st>>>(
+        c->hw_rec, c->hc_rec, c->rec_B, c->dims - c->rec_k0, c->ng, c->map_w + m0,
+        c->map_counts + m0, c->status);
   } else if (c->smem_hist) {
     hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
         c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
@@ -732,12 +738,21 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
                      : (c->smem_hist && spec) ? LAYOUT_EDGES
                                               : LAYOUT_RUNTIME;
   c->layout = layout;
+  // a records-layout fill with d >= 12 histograms its first REC_K0 axes in
+  // the shared memory left next to the edges (fill.cuh K0)
+  if (layout == LAYOUT_RECORDS && c->dims >= 12) {
+    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, 0, REC_K0);
+    if (b > (size_t)optin) return bail(fail(VPB_ERR_UNSUPPORTED, "records layout does not fit"));
+    c->rec_k0 = REC_K0;
+    c->hs = REC_K0;
+    c->smem = b;
+  }
   int per_sm = 0;
   if (fill_occupancy(c->id, c->dims, layout, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
     return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
   c->grid = sms * per_sm;
   if (c->records) {
-    c->n_groups = (c->dims + 7) / 8;
+    c->n_groups = (c->dims - c->rec_k0 + 7) / 8;
     const long long cap_runs = c->ntiles_cap * FILL_TILE;
     const long long per_rec = 8 + 16 * (long long)c->n_groups;
     // records per chunk: 1/16 of the iteration's records, within [256 MiB,
@@ -766,6 +781,10 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     A(c->rec_w2, (size_t)c->rec_ch);
     A(c->hw_rec, (size_t)c->n_groups * c->rec_B * c->ng * 8);
     A(c->hc_rec, (size_t)c->n_groups * c->rec_B * c->ng * 8);
+    if (c->rec_k0 > 0) {
+      A(c->hw_part, (size_t)c->grid * c->rec_k0 * c->ng);
+      A(c->hc_part, (size_t)c->grid * c->rec_k0 * c->ng);
+    }
   } else if (c->smem_hist) {
     A(c->hw_part, (size_t)c->grid * m);
     A(c->hc_part, (size_t)c->grid * m);
@@ -971,7 +990,7 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   // plan_scan, plan_offsets, fill | chunks x (fill + groups), fixup, histogram
   // reduce, cube_terms, results_leaf, results_tree, alloc, refine, step, mark
   const int fill = c->records ? c->n_chunks * (1 + c->n_groups) : 1;
-  if (launches) *launches = 2 + fill + 2 + 3 + 1 + 1 + 2;
+  if (launches) *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 2;
   return VPB_OK;
 }
 

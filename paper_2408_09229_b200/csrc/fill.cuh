@@ -46,6 +46,7 @@ constexpr int FILL_NT = VPB_FILL_NT;    // threads per CTA (one CTA per SM)
 constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per lane per tile
 constexpr int FILL_TILE = 32 * FILL_RPT;   // runs per warp tile
 constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
+constexpr int REC_K0 = 4;   // axes kept in shared memory by a records-layout fill (d >= 12)
 
 // Per-iteration schedule written by the plan kernels (device memory).
 struct Sched {
@@ -141,6 +142,9 @@ constexpr int LAYOUT_RUNTIME = 3;   // generic kernel: a.smem_hist / a.records /
 template <int ID, int D, int LAYOUT>
 __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
+  // records layout with many axes: the first K0 axes are histogrammed in this
+  // kernel's spare shared memory (next to the edges), the rest go to records
+  constexpr int K0 = (LAYOUT == LAYOUT_RECORDS && D >= 12) ? REC_K0 : 0;
   // cube digits RN(digit/N) per axis in registers for small d; above that the
   // digits are kept packed and RN(digit/N) is read from the shared table
   constexpr bool DQ_REG = D == 0 || D <= 12;
@@ -310,12 +314,12 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           if constexpr (LAYOUT == LAYOUT_RECORDS) {
             // the axis group is complete: store its intervals now, so they
             // are not live across the integrand
-            if ((j & 7) == 7 || j == D - 1) {
-              const int g = j >> 3;
+            if (j >= K0 && (((j - K0) & 7) == 7 || j == D - 1)) {
+              const int g = (j - K0) >> 3;   // records hold axes K0 + 8g ..
               uint32_t wv[4];
 #pragma unroll
               for (int q = 0; q < 4; q++) {
-                const int j0 = 8 * g + 2 * q, j1 = j0 + 1;
+                const int j0 = K0 + 8 * g + 2 * q, j1 = j0 + 1;
                 const uint32_t lo16 = j0 <= j ? (uint32_t)iv[j0 <= j ? j0 : 0] : 0u;
                 const uint32_t hi16 = j1 <= j ? (uint32_t)iv[j1 <= j ? j1 : 0] : 0u;
                 wv[q] = lo16 | (hi16 << 16);
@@ -340,6 +344,27 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           constexpr bool RT = LAYOUT == LAYOUT_RUNTIME;
           if (LAYOUT == LAYOUT_RECORDS) {
             a.rec_w2[(T0 - rec0) + rr * 32 + lane] = w2;   // intervals stored while sampling
+            if constexpr (K0 > 0) {
+              // axes 0..K0-1 here, lane-rotated as below
+              const int rot = lane % K0;
+              int idx[K0];
+#pragma unroll
+              for (int j = 0; j < K0; j++) idx[j] = iv[j] * hs + j;
+#pragma unroll
+              for (int b = 1; b < K0; b <<= 1) {
+                const bool on = (rot & b) != 0;
+                int t[K0];
+#pragma unroll
+                for (int j = 0; j < K0; j++) t[j] = on ? idx[(j + b) % K0] : idx[j];
+#pragma unroll
+                for (int j = 0; j < K0; j++) idx[j] = t[j];
+              }
+#pragma unroll
+              for (int j = 0; j < K0; j++) {
+                atomicAdd(&s_hw[idx[j]], w2);
+                atomicAdd(&s_hc[idx[j]], 1u);
+              }
+            }
           } else if (RT && a.records) {
             // deferred to hist_records_kernel: w^2 and the intervals, 8 axes
             // per 16-byte group (coalesced over a warp's RPT-strided rows)
@@ -470,12 +495,15 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
 
   if (a.smem_hist) {
     __syncthreads();
-    double *hw = a.hw_part + (size_t)blockIdx.x * d * ng;
-    unsigned *hc = a.hc_part + (size_t)blockIdx.x * d * ng;
-    for (int i = tid; i < d * ng; i += FILL_NT) {   // back to [axis][interval]
+    const int nh = LAYOUT == LAYOUT_RECORDS ? K0 : d;   // axes histogrammed here
+    double *hw = a.hw_part + (size_t)blockIdx.x * nh * ng;
+    unsigned *hc = a.hc_part + (size_t)blockIdx.x * nh * ng;
+    // records layout: the chunks of an iteration add into the CTA's slice
+    const bool acc = LAYOUT == LAYOUT_RECORDS && a.tile_lo > 0;
+    for (int i = tid; i < nh * ng; i += FILL_NT) {   // back to [axis][interval]
       const int j = i / ng, b = i - j * ng;
-      hw[i] = s_hw[b * hs + j];
-      hc[i] = s_hc[b * hs + j];
+      hw[i] = acc ? __dadd_rn(hw[i], s_hw[b * hs + j]) : s_hw[b * hs + j];
+      hc[i] = acc ? hc[i] + s_hc[b * hs + j] : s_hc[b * hs + j];
     }
   }
 }

@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(HR_NT, 2)
 __global__ void rec_reduce_kernel(const double *hw_rec, const unsigned *hc_rec, int nparts,
                                   int dims, int ng, double *map_w, long long *map_counts,
                                   const int *status) {
+  // dims = axes in the records (the map rows after the fill's own k0 axes;
+  // map_w / map_counts point at row k0)
   __shared__ double sw[8][33];
   __shared__ long long sc[8][33];
   if (*status & 1) return;
