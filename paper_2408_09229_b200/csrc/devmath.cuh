@@ -88,7 +88,8 @@ template <class EdgeFn>
 __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2, double rns2,
                                               double ngf, int ng, EdgeFn edge, double &jac,
                                               int &iv) {
-  const uint32_t whi = (uint32_t)(w >> 32), wlo = (uint32_t)w;
+  uint32_t whi, wlo;   // split opaquely: keeps the bit-63 test a 32-bit compare
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(wlo), "=r"(whi) : "l"(w));
   const double up = __hiloint2double((int)(((whi >> 11) & 0xFFFFFu) | 0x3FF00000u),
                                      (int)__funnelshift_r(wlo, whi, 11));
   const double cm = __hiloint2double((~(int)whi >> 31) & 0x3FF00000, 0);   // 1 - bit63

@@ -195,9 +195,47 @@ def test_fill_matches_oracle(name, dims, ng, ns, nh):
     ref = O.fill(off, edges, ns, seed, batch, rb, name)
     np.testing.assert_array_equal(got[1], ref[1])   # map counts
     np.testing.assert_array_equal(got[4], ref[4])   # cube counts
-    np.testing.assert_allclose(got[0], ref[0], rtol=1e-12, atol=1e-300)
-    np.testing.assert_allclose(got[2], ref[2], rtol=1e-12, atol=1e-290)
-    np.testing.assert_allclose(got[3], ref[3], rtol=1e-12, atol=1e-290)
+    # the Asian payoff max(S - K, 0) cancels near the strike (device vs libm
+    # exp/erfc differ by ulps of S ~ 100): absolute floor relative to the scale
+    fl = (lambda a: 1e-13 * np.abs(a).max()) if name == "asian_option" else (lambda a: 1e-290)
+    np.testing.assert_allclose(got[0], ref[0], rtol=1e-12, atol=max(1e-300, fl(ref[0])))
+    np.testing.assert_allclose(got[2], ref[2], rtol=1e-12, atol=fl(ref[2]))
+    np.testing.assert_allclose(got[3], ref[3], rtol=1e-12, atol=fl(ref[3]))
+
+
+@pytest.mark.parametrize("name,dims,ng,ns,nh", [
+    ("gaussian", 5, 40, 3, (2, 60)),            # generic kernel, odd d (Philox stride d+1)
+    ("gaussian", 7, 33, 2, (10, 300)),          # generic kernel, odd d, odd ng
+    ("gaussian", 1, 17, 9, (2, 200)),           # generic kernel, d = 1
+    ("asian_option", 16, 128, 2, (2, 40)),      # d=16 registry default: records + K0 axes
+    ("path_integral", 7, 96, 2, (20, 200)),     # d=7, odd: pair table
+])
+def test_fill_more_geometries(name, dims, ng, ns, nh):
+    test_fill_matches_oracle(name, dims, ng, ns, nh)
+
+
+@pytest.mark.parametrize("name,dims,n_eval,max_it,ng", [
+    ("asian_option", 16, 60_000, 4, 64),
+    ("path_integral", 7, 50_000, 5, 128),
+    ("exponential", 10, 40_000, 4, 1024),       # d=10 at ng=1024: unpadded histogram stride
+])
+def test_integrate_trajectory_matches_oracle(name, dims, n_eval, max_it, ng):
+    # the whole device iteration (plan, fill, results, allocation, refine)
+    # against the oracle's restated loop on the application integrands
+    spec = P.lookup(name)
+    bounds = list(spec.bounds)
+    with P.Integrator(spec.evaluate_batch, bounds,
+                      P.IntegratorConfig(n_eval=n_eval, max_it=max_it, n_intervals=ng,
+                                         seed=13, batch_size=4096)) as it:
+        it.iterate(max_it)
+        est, var, evals = it.history()
+        edges = it.edges()
+    ref = O.integrate(name, bounds, n_eval, max_it=max_it, n_intervals=ng, seed=13,
+                      batch_size=4096, params=spec.evaluate_batch.params(dims))
+    np.testing.assert_array_equal(evals, ref.evals)
+    np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
+    np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
+    np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=1e-13)
 
 
 @pytest.mark.parametrize("layout,chunk", [("records", "2048"), ("records", ""), ("global", "")])
