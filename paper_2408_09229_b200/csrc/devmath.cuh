@@ -101,8 +101,10 @@ __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2
   ylo = (yhi >= 0x3FF00000) ? -1 : ylo;                                     // y >= 1 ->
   yhi = min(yhi, 0x3FEFFFFF);                                               // 0x3FEFFFFFFFFFFFFF
   const double t = __dmul_rn(__hiloint2double(yhi, ylo), ngf);
-  const int ivj = min(__double2loint(__dadd_rz(t, 4503599627370496.0)), ng - 1);
-  const double fiv = __dadd_rn(__hiloint2double(0x43300000, ivj), -4503599627370496.0);
+  const double sh = __dadd_rz(t, 4503599627370496.0);   // 2^52 + trunc(t)
+  const int ivj = min(__double2loint(sh), ng - 1);
+  // 2^52 + iv has the shifter's high word (0x43300000): reuse that register
+  const double fiv = __dadd_rn(__hiloint2double(__double2hiint(sh), ivj), -4503599627370496.0);
   const double frac = __dadd_rn(t, -fiv);
   double elo, dx;
   edge(ivj, elo, dx);
