@@ -384,6 +384,13 @@ class Integrator:
                                        N.ptr(cnt)))
         return mw, mc, s1, s2, cnt
 
+    def set_shard(self, world: int, rank: int):
+        """Fill only rank's share of each plan (vp/executor.py:41-57 rule)
+        without a communicator: the caller merges the accumulators (what the
+        NCCL all-reduce does in a distributed run)."""
+        N.check(self._lib.vpb_set_shard(self._ctx, int(world), int(rank)), "vpb_set_shard")
+        self.world, self.rank = int(world), int(rank)
+
     def fill(self, run_base: int):
         rc = self._lib.vpb_fill(self._ctx, int(run_base))
         if rc == N.VPB_ERR_NONFINITE:

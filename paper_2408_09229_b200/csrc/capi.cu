@@ -1169,7 +1169,7 @@ namespace {
 template <class T>
 struct DBuf {
   T *p = nullptr;
-  ~DBuf() { if (p) cudaFree(p); }
+  ~DBuf() { cached_free(p); }   // callers synchronise before returning
   int alloc(size_t n) { return dalloc(&p, n); }
   int up(const T *h, size_t n) {
     TRY(alloc(n));

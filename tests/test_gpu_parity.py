@@ -280,6 +280,30 @@ def test_fill_shards_sum_to_whole():
     np.testing.assert_allclose(sum(p[2] for p in parts), whole[2], rtol=1e-12, atol=1e-290)
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_iteration_shards_merge_to_whole(world):
+    # the distributed data path without NCCL: each rank's context plans the
+    # whole iteration, fills its shard [lo, hi) (computed on device by the
+    # reference's partition rule) and the summed accumulators -- what the
+    # per-iteration all-reduce produces -- equal the single-GPU fill
+    cfg = P.IntegratorConfig(n_eval=300_000, max_it=3, n_intervals=64, seed=21, batch_size=4096)
+
+    def run(w, r):
+        with P.Integrator("multipeak8", [(0.0, 1.0)] * 8, cfg) as it:
+            if w > 1:
+                it.set_shard(w, r)
+            it.fill(123_457)
+            return it.accumulators()
+
+    whole = run(1, 0)
+    parts = [run(world, r) for r in range(world)]
+    np.testing.assert_array_equal(sum(p[1] for p in parts), whole[1])   # map counts
+    np.testing.assert_array_equal(sum(p[4] for p in parts), whole[4])   # cube counts
+    np.testing.assert_allclose(sum(p[0] for p in parts), whole[0], rtol=1e-12)
+    np.testing.assert_allclose(sum(p[2] for p in parts), whole[2], rtol=1e-12, atol=1e-290)
+    np.testing.assert_allclose(sum(p[3] for p in parts), whole[3], rtol=1e-12, atol=1e-290)
+
+
 @pytest.mark.parametrize("traj,name", [("traj_gauss4_small.npz", "gaussian"),
                                        ("traj_ridge_small.npz", "ridge"),
                                        ("traj_genzosc_small.npz", "genz_oscillatory6"),
