@@ -122,6 +122,15 @@ struct EdgeRow {
     dx = __dadd_rn(e[i + 1], -lo);
   }
 };
+template <int RS>   // pair table laid out [interval][axis], RS axes per row
+struct EdgePairsT {
+  const double2 *p;   // points at the axis column
+  __device__ __forceinline__ void operator()(int i, double &lo, double &dx) const {
+    const double2 v = p[i * RS];
+    lo = v.x;
+    dx = v.y;
+  }
+};
 struct EdgePairs {
   const double2 *p;
   __device__ __forceinline__ void operator()(int i, double &lo, double &dx) const {

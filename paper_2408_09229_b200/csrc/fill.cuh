@@ -46,6 +46,9 @@ constexpr int FILL_NT = VPB_FILL_NT;    // threads per CTA (one CTA per SM)
 constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per lane per tile
 constexpr int FILL_TILE = 32 * FILL_RPT;   // runs per warp tile
 constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
+#ifndef VPB_DQ_REG_MAX
+#define VPB_DQ_REG_MAX 12   // dims up to which RN(digit/N) stays in registers
+#endif
 constexpr int REC_K0 = 4;   // axes kept in shared memory by a records-layout fill (d >= 12)
 
 // Per-iteration schedule written by the plan kernels (device memory).
@@ -139,6 +142,16 @@ constexpr int LAYOUT_PAIRS = 1;     // pair table + shared histograms
 constexpr int LAYOUT_RECORDS = 2;   // edge rows + records (hist.cuh)
 constexpr int LAYOUT_RUNTIME = 3;   // generic kernel: a.smem_hist / a.records / global atomics
 
+// Integrands whose value does not depend on the order of the axes (up to the
+// rounding of their sums/products): the fill may hand them the coordinates
+// in a lane-dependent axis order (XPERM below).
+template <int ID>
+__host__ __device__ constexpr bool axis_symmetric() {
+  return ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_RIDGE || ID == VPB_LINEAR ||
+         ID == VPB_COSINE || ID == VPB_EXPONENTIAL || ID == VPB_ROOS_ARNOLD ||
+         ID == VPB_MOROKOFF || ID == VPB_ASIAN_OPTION || ID == VPB_CONSTANT;
+}
+
 template <int ID, int D, int LAYOUT>
 __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
@@ -147,7 +160,18 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   constexpr int K0 = (LAYOUT == LAYOUT_RECORDS && D >= 12) ? REC_K0 : 0;
   // cube digits RN(digit/N) per axis in registers for small d; above that the
   // digits are kept packed and RN(digit/N) is read from the shared table
-  constexpr bool DQ_REG = D == 0 || D <= 12;
+  constexpr bool DQ_REG = D == 0 || D <= VPB_DQ_REG_MAX;
+  // XPERM (power-of-two d, pair table, axis-symmetric integrand): at step s
+  // lane l samples axis s ^ (l mod d).  The 8 lanes of a quarter-warp then
+  // read 8 different axes, and with the pair table laid out [interval][axis]
+  // (128-byte rows for d = 8) their 16-byte loads land in 8 different bank
+  // quads -- conflict-free instead of ~10 wavefronts per LDS.128 for random
+  // intervals of one axis.  Steps 2k, 2k+1 still cover one Philox block
+  // (k ^ (l>>1)), so only the word order flips; the histogram updates are
+  // already lane-spread (no barrel rotation); x and the Jacobian factors
+  // reach the integrand in permuted order (bitwise the same coordinates; sums
+  // and products round in a different order, within the parity tolerance).
+  constexpr bool XPERM = PAIRS && (D == 2 || D == 4 || D == 8) && axis_symmetric<ID>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
@@ -179,7 +203,8 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     for (int i = tid; i < d * ng; i += FILL_NT) {
       const int j = i / ng, b = i - j * ng;
       const double lo = a.edges[j * (ng + 1) + b];
-      s_pair[i] = make_double2(lo, __dadd_rn(a.edges[j * (ng + 1) + b + 1], -lo));
+      // [axis][interval], or [interval][axis] for XPERM
+      s_pair[XPERM ? b * D + j : i] = make_double2(lo, __dadd_rn(a.edges[j * (ng + 1) + b + 1], -lo));
     }
   } else {
     for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
@@ -200,6 +225,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
 
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = FILL_NT / 32;
+  const int xr = XPERM ? (lane & (D - 1)) : 0;   // XPERM: step s samples axis s ^ xr
   const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
   // this warp's tiles: [L + w*P + b, min(L + (w+1)*P, U)) in steps of the grid,
   // [L, U) = the launch's tile range
@@ -256,6 +282,19 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           if constexpr (DQ_REG) dq[j] = dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
           else dpk |= (uint64_t)dig << (j * dbits);
         }
+        if constexpr (XPERM && DQ_REG) {   // dq[s] <- dq[s ^ xr]: butterfly over the bits of xr
+#pragma unroll
+          for (int b = 1; b < D; b <<= 1) {
+            const bool on = (xr & b) != 0;
+#pragma unroll
+            for (int j = 0; j < D; j++)
+              if ((j & b) == 0) {
+                const double lo_ = dq[j], hi_ = dq[j | b];
+                dq[j] = on ? hi_ : lo_;
+                dq[j | b] = on ? lo_ : hi_;
+              }
+          }
+        }
       };
       // RN(digit_j / N) of the current cube
       auto dq_of = [&](int j) -> double {
@@ -298,6 +337,22 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
         int iv[MAXD];
         double jac = 1.0;
         uint64_t w0 = 0, w1 = 0;
+        if constexpr (XPERM) {
+#pragma unroll
+          for (int k2 = 0; k2 < D / 2; k2++) {
+            const unsigned long long blk = base + (unsigned long long)(k2 ^ (xr >> 1));
+            philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+                   w0, w1);
+            const uint64_t wa = (xr & 1) ? w1 : w0, wb = (xr & 1) ? w0 : w1;
+            const int s0 = 2 * k2, s1 = s0 + 1;
+            const double dq0 = DQ_REG ? dq[DQ_REG ? s0 : 0] : dq_of(s0 ^ xr);
+            const double dq1 = DQ_REG ? dq[DQ_REG ? s1 : 0] : dq_of(s1 ^ xr);
+            x[s0] = sample_axis(wa, dq0, nsf2, rns2, a.ngf, ng,
+                                EdgePairsT<D>{s_pair + (s0 ^ xr)}, jac, iv[s0]);
+            x[s1] = sample_axis(wb, dq1, nsf2, rns2, a.ngf, ng,
+                                EdgePairsT<D>{s_pair + (s1 ^ xr)}, jac, iv[s1]);
+          }
+        } else {
 #pragma unroll
         for (int j = 0; j < (D > 0 ? D : d); j++) {
           if ((j & 1) == 0) {
@@ -330,6 +385,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             }
           }
         }
+        }   // !XPERM
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         const double f = integrand<ID, D>(x, d, a.P);
         if (!isfinite(f)) {
@@ -393,11 +449,12 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
             // retry; rotated, a step's lanes are spread over d histograms.
             const int rot = lane % d;
             // flat histogram index of each axis, rotated so that slot s holds
-            // axis (s + rot) mod d
+            // axis (s + rot) mod d (XPERM: step s already holds axis s ^ xr)
             int idx[MAXD];
 #pragma unroll
-            for (int j = 0; j < (D > 0 ? D : d); j++) idx[j] = iv[j] * hs + j;
-            if constexpr (D > 1) {
+            for (int j = 0; j < (D > 0 ? D : d); j++) idx[j] = iv[j] * hs + (XPERM ? (j ^ xr) : j);
+            if constexpr (XPERM) {
+            } else if constexpr (D > 1) {
 #pragma unroll
               for (int b = 1; b < D; b <<= 1) {   // barrel rotation by rot
                 const bool on = (rot & b) != 0;
