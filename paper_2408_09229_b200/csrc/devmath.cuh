@@ -245,6 +245,33 @@ __device__ __forceinline__ double pw_sum(const double *a) {
   }
 }
 
+// numpy's pairwise sum of N terms (8 <= N <= 128) accumulated as the terms
+// arrive in index order: the 8 accumulators r[k] = a[k] + a[k+8] + ... are
+// complete once a[full-1] is in (full = N - N%8), then the tree combines
+// them and the tail a[full..N) is added in order -- bit-identical to
+// pw_sum<N>, with only 8 partial sums live instead of N terms.
+template <int N>
+struct PairwiseAcc {
+  static_assert(N >= 8 && N <= 128, "one numpy leaf");
+  static constexpr int FULL = N - (N % 8);
+  double r[8];
+  double res;
+  // j is the term index; called from fully unrolled loops, so every branch
+  // folds at compile time
+  __device__ __forceinline__ void add(int j, double v) {
+    if (j < 8) {
+      r[j] = v;
+    } else if (j < FULL) {
+      r[j % 8] = __dadd_rn(r[j % 8], v);
+    } else {
+      res = __dadd_rn(res, v);
+    }
+    if (j == FULL - 1)
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  }
+};
+
 // Runtime-length version (recursion unrolled with an explicit stack).
 __device__ __forceinline__ double pw_leaf(const double *a, long long n) {
   if (n < 8) {

@@ -152,8 +152,17 @@ __host__ __device__ constexpr bool axis_symmetric() {
          ID == VPB_MOROKOFF || ID == VPB_ASIAN_OPTION || ID == VPB_CONSTANT;
 }
 
+// Threads per CTA: FILL_NT (640: 96 registers), or 768 (80 registers) for
+// the many-axis records kernels, whose streamed sums fit in 80 registers
+// and which gain from the fifth and sixth warp per scheduler (cfg5 -3%).
 template <int ID, int D, int LAYOUT>
-__global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
+__host__ __device__ constexpr int fill_nt() {
+  return (LAYOUT == LAYOUT_RECORDS && D > 12) ? 768 : FILL_NT;
+}
+
+template <int ID, int D, int LAYOUT>
+__global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(const FillArgs a) {
+  constexpr int NT = fill_nt<ID, D, LAYOUT>();
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
   // records layout with many axes: the first K0 axes are histogrammed in this
   // kernel's spare shared memory (next to the edges), the rest go to records
@@ -172,6 +181,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   // reach the integrand in permuted order (bitwise the same coordinates; sums
   // and products round in a different order, within the parity tolerance).
   constexpr bool XPERM = PAIRS && (D == 2 || D == 4 || D == 8) && axis_symmetric<ID>();
+  // STREAM (the Gaussian at 8 < d <= 128, e.g. cfg5): the integrand's
+  // pairwise sum of (x_j - mu)^2 is accumulated while the axes are sampled
+  // (PairwiseAcc, bit-identical to the row sum), so neither x[] nor the d
+  // squared terms are live across the sampling loop -- ~2d fewer registers
+  constexpr bool STREAM = ID == VPB_GAUSSIAN && D > 8 && D <= 128 && !XPERM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
@@ -200,19 +214,19 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
 
   if constexpr (PAIRS) {
-    for (int i = tid; i < d * ng; i += FILL_NT) {
+    for (int i = tid; i < d * ng; i += NT) {
       const int j = i / ng, b = i - j * ng;
       const double lo = a.edges[j * (ng + 1) + b];
       // [axis][interval], or [interval][axis] for XPERM
       s_pair[XPERM ? b * D + j : i] = make_double2(lo, __dadd_rn(a.edges[j * (ng + 1) + b + 1], -lo));
     }
   } else {
-    for (int i = tid; i < d * (ng + 1); i += FILL_NT) s_edges[i] = a.edges[i];
+    for (int i = tid; i < d * (ng + 1); i += NT) s_edges[i] = a.edges[i];
   }
   if (a.smem_hist)
-    for (int i = tid; i < hs * ng; i += FILL_NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
+    for (int i = tid; i < hs * ng; i += NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
   if (dq_tab)
-    for (int i = tid; i < a.n_strat; i += FILL_NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
+    for (int i = tid; i < a.n_strat; i += NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
 
   if (tid == 0) s_flag[0] = *a.status;   // an earlier iteration failed: nothing to fill
   const Sched S = *a.sched;
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
   if (s_flag[0]) return;   // block-uniform
 
   const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = FILL_NT / 32;
+  constexpr int NW = NT / 32;
   const int xr = XPERM ? (lane & (D - 1)) : 0;   // XPERM: step s samples axis s ^ xr
   const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
   // this warp's tiles: [L + w*P + b, min(L + (w+1)*P, U)) in steps of the grid,
@@ -333,6 +347,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           load_digits(cube);
         }
         // ---- sample (vp/kernels.py:59-88)
+        PairwiseAcc<STREAM ? D : 8> gacc;
         double x[MAXD];
         int iv[MAXD];
         double jac = 1.0;
@@ -366,6 +381,10 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
           else
             x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
                                EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j]);
+          if constexpr (STREAM) {   // vp/integrands.py:135-139 term (x_j - mu)^2
+            const double u = __dadd_rn(x[j], -a.P.p[0]);
+            gacc.add(j, __dmul_rn(u, u));
+          }
           if constexpr (LAYOUT == LAYOUT_RECORDS) {
             // the axis group is complete: store its intervals now, so they
             // are not live across the integrand
@@ -387,7 +406,11 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
         }
         }   // !XPERM
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
-        const double f = integrand<ID, D>(x, d, a.P);
+        double f;
+        if constexpr (STREAM)   // integrands.cuh VPB_GAUSSIAN on the streamed sum
+          f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gacc.res, a.P.p[3], a.P.p[4])));
+        else
+          f = integrand<ID, D>(x, d, a.P);
         if (!isfinite(f)) {
           atomicMin(a.err_run, (unsigned long long)(r0 + rr));
           atomicOr(a.status, 1);
@@ -557,7 +580,7 @@ __global__ void __launch_bounds__(FILL_NT, 1) fill_kernel(const FillArgs a) {
     unsigned *hc = a.hc_part + (size_t)blockIdx.x * nh * ng;
     // records layout: the chunks of an iteration add into the CTA's slice
     const bool acc = LAYOUT == LAYOUT_RECORDS && a.tile_lo > 0;
-    for (int i = tid; i < nh * ng; i += FILL_NT) {   // back to [axis][interval]
+    for (int i = tid; i < nh * ng; i += NT) {   // back to [axis][interval]
       const int j = i / ng, b = i - j * ng;
       hw[i] = acc ? __dadd_rn(hw[i], s_hw[b * hs + j]) : s_hw[b * hs + j];
       hc[i] = acc ? hc[i] + s_hc[b * hs + j] : s_hc[b * hs + j];

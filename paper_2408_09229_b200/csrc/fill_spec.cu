@@ -15,7 +15,7 @@ cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  fill_kernel<ID, D, LAYOUT><<<grid, FILL_NT, smem, st>>>(a);
+  fill_kernel<ID, D, LAYOUT><<<grid, (fill_nt<ID, D, LAYOUT>()), smem, st>>>(a);
   return cudaGetLastError();
 }
 template <int ID, int D, int LAYOUT>
@@ -23,7 +23,7 @@ cudaError_t occ_one(size_t smem, int *ctas) {
   cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, LAYOUT>, FILL_NT,
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, LAYOUT>, fill_nt<ID, D, LAYOUT>(),
                                                        smem);
 }
 }  // namespace
