@@ -278,6 +278,11 @@ struct vpb_ctx {
   // timing
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
+  // side stream: the histogram reduction and the map refinement run there,
+  // concurrently with the cube-chain fixup and the results/allocation chain
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_open = false;   // side holds work not yet joined into st
   int it_enq = 0;   // iterations enqueued since reset
   // one iteration captured as a CUDA graph (launched once per iteration;
   // the six phase-event nodes are re-pointed at the iteration's events)
@@ -363,7 +368,26 @@ int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
   return VPB_OK;
 }
 
-int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr) {
+// st -> side dependency (side continues after everything enqueued on st)
+int fork_side(vpb_ctx *c) {
+  CK(cudaEventRecord(c->ev_fork, c->st));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  c->side_open = true;
+  return VPB_OK;
+}
+// side -> st dependency (st continues after everything enqueued on side)
+int join_side(vpb_ctx *c) {
+  if (!c->side_open) return VPB_OK;
+  CK(cudaEventRecord(c->ev_join, c->side));
+  CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+  c->side_open = false;
+  return VPB_OK;
+}
+
+// join_after: join the side stream before returning (host entry points and
+// the multi-GPU all-reduce); the iteration body defers it to the update.
+int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr,
+                 bool defer_join = false) {
   const size_t m = (size_t)c->dims * c->ng;
   CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
   if (!c->smem_hist && !c->records) {
@@ -403,25 +427,28 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   if (k1) CK(rec_event(c, k1));
   if (timed) CK(cudaEventRecord(c->f1, c->st));
   const long long nt = c->ntiles_cap;
+  TRY(fork_side(c));   // histogram reduction (side) || cube-chain fixup (st)
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
+  cudaStream_t hs_st = c->side;
   if (c->records) {
     const size_t m0 = (size_t)c->rec_k0 * c->ng;   // rows histogrammed by the fill itself
     if (m0 > 0)
-      hist_reduce_kernel<<<(unsigned)((m0 + 31) / 32), dim3(32, 8), 0, c->st>>>(
+      hist_reduce_kernel<<<(unsigned)((m0 + 31) / 32), dim3(32, 8), 0, hs_st>>>(
           c->hw_part, c->hc_part, c->grid, (long long)m0, c->map_w, c->map_counts);
-    rec_reduce_kernel<<<(unsigned)((m - m0 + 31) / 32), dim3(32, 8), 0, c->st>>>(
+    rec_reduce_kernel<<<(unsigned)((m - m0 + 31) / 32), dim3(32, 8), 0, hs_st>>>(
         c->hw_rec, c->hc_rec, c->rec_B, c->dims - c->rec_k0, c->ng, c->map_w + m0,
         c->map_counts + m0, c->status);
   } else if (c->smem_hist) {
-    hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
+    hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, hs_st>>>(
         c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
   } else {
-    CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, c->st));
-    hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, c->st>>>(c->hc_glob,
+    CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, hs_st));
+    hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, hs_st>>>(c->hc_glob,
                                                                            (long long)m,
                                                                            c->map_counts);
   }
   CK(cudaGetLastError());
+  if (!defer_join || c->comm) TRY(join_side(c));
   if (c->comm) {
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->accf, c->accf, m + 2 * (size_t)c->n_cubes, ncclFloat64, ncclSum, c->comm,
@@ -435,6 +462,11 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
 int enqueue_update(vpb_ctx *c, int record) {
   const double V = 1.0 / (double)c->n_cubes;
   const PwPlanDev pd = c->pw.dev();
+  // map refinement (side, after the histogram reduction already queued there
+  // or after the all-reduce) || results + allocation (st)
+  if (!c->side_open) TRY(fork_side(c));
+  refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->side>>>(
+      c->edges, c->map_w, c->map_counts, c->ng, c->alpha, c->refine_scr, c->status, nullptr);
   cube_terms_kernel<<<(unsigned)((c->n_cubes + 255) / 256), 256, 0, c->st>>>(
       c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, c->pwterms, c->status);
   results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
@@ -445,9 +477,8 @@ int enqueue_update(vpb_ctx *c, int record) {
   alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, c->beta,
                                                        (double)c->n_eval, c->uniform_nh, c->sc, 0,
                                                        c->n_h, c->bsum, c->status);
-  refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->st>>>(c->edges, c->map_w, c->map_counts, c->ng, c->alpha,
-                                            c->refine_scr, c->status, nullptr);
   CK(cudaGetLastError());
+  TRY(join_side(c));
   return VPB_OK;
 }
 
@@ -465,7 +496,7 @@ int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
   CK(rec_event(c, E[0]));
   TRY(enqueue_plan(c, 1, nullptr));
   CK(rec_event(c, E[1]));
-  TRY(enqueue_fill(c, false, E[2], E[3]));
+  TRY(enqueue_fill(c, false, E[2], E[3], /*defer_join=*/true));
   CK(rec_event(c, E[4]));
   TRY(enqueue_update(c, 1));
   CK(rec_event(c, E[5]));
@@ -567,6 +598,10 @@ void free_ctx(vpb_ctx *c) {
       if (e) cudaEventDestroy(e);
   if (c->f0) cudaEventDestroy(c->f0);
   if (c->f1) cudaEventDestroy(c->f1);
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
@@ -799,6 +834,10 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
       if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(VPB_ERR_CUDA, "event creation"));
   if (cudaEventCreate(&c->f0) != cudaSuccess || cudaEventCreate(&c->f1) != cudaSuccess)
     return bail(fail(VPB_ERR_CUDA, "event creation"));
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(VPB_ERR_CUDA, "side stream creation"));
   if ((rc = vpb_reset(c)) != VPB_OK) return bail(rc);
   *out = c;
   return VPB_OK;
