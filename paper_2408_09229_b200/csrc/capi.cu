@@ -350,6 +350,14 @@ cudaError_t rec_event(vpb_ctx *c, cudaEvent_t e) {
                       : cudaEventRecord(e, c->st);
 }
 
+// A compile-time (integrand, dims) kernel exists and applies: the 3-peak
+// streamed sum of the multipeak kernels needs the registry's 3 peaks.
+bool specialisable(const vpb_ctx *c) {
+  if (!fill_is_specialised(c->id, c->dims)) return false;
+  if (c->id == VPB_MULTIPEAK && c->P.p[0] != 3.0) return false;
+  return true;
+}
+
 int setdev(vpb_ctx *c) {
   CK(cudaSetDevice(c->dev));
   return VPB_OK;
@@ -743,7 +751,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   const char *force = std::getenv("VPB_FILL_LAYOUT");
   const std::string forced = force ? force : "";
   c->smem_hist = forced != "records" && forced != "global";
-  c->pairs = c->smem_hist && forced != "edges" && fill_is_specialised(c->id, c->dims) &&
+  c->pairs = c->smem_hist && forced != "edges" && specialisable(c) &&
              !getenv("VPB_NO_PAIRS");
   // shared-histogram candidates in order: (pairs, padded stride), (pairs,
   // stride d), (edge rows, padded), (edge rows, stride d)
@@ -767,7 +775,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // shared-memory histograms per 8-axis group), else global atomics
   c->records = !c->smem_hist && forced != "global" && c->ng <= 65535 &&
                hist_records_smem(c->ng) <= (size_t)optin;
-  const bool spec = fill_is_specialised(c->id, c->dims);
+  const bool spec = specialisable(c);
   const int layout = (c->records && spec)     ? LAYOUT_RECORDS
                      : c->pairs               ? LAYOUT_PAIRS
                      : (c->smem_hist && spec) ? LAYOUT_EDGES

@@ -272,6 +272,41 @@ struct PairwiseAcc {
   }
 };
 
+// numpy's pairwise sum of N terms accumulated in index order with few live
+// partials, bit-identical to pw_sum<N> (fully unrolled callers: all branches
+// fold):  N < 8 sequential from 0.0;  8 <= N < 16 the 8-leaf tree
+// ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) combined pair by pair (3 partials live),
+// then the tail;  16 <= N <= 128 PairwiseAcc (8 partials).
+template <int N>
+struct StreamSum {
+  static_assert(N >= 1 && N <= 128, "one numpy leaf");
+  double p0, p1, q0, res;
+  PairwiseAcc<(N >= 16 ? N : 16)> big;
+  __device__ __forceinline__ void add(int j, double v) {
+    if constexpr (N < 8) {
+      res = (j == 0) ? __dadd_rn(0.0, v) : __dadd_rn(res, v);
+    } else if constexpr (N < 16) {
+      if (j >= 8) { res = __dadd_rn(res, v); return; }
+      switch (j & 3) {
+        case 0: p0 = v; break;
+        case 1: p0 = __dadd_rn(p0, v); break;
+        case 2: p1 = v; break;
+        default: {
+          const double q = __dadd_rn(p0, __dadd_rn(p1, v));
+          if (j == 3) q0 = q;
+          else res = __dadd_rn(q0, q);
+        }
+      }
+    } else {
+      big.add(j, v);
+    }
+  }
+  __device__ __forceinline__ double result() const {
+    if constexpr (N >= 16) return big.res;
+    else return res;
+  }
+};
+
 // Runtime-length version (recursion unrolled with an explicit stack).
 __device__ __forceinline__ double pw_leaf(const double *a, long long n) {
   if (n < 8) {

@@ -153,11 +153,16 @@ __host__ __device__ constexpr bool axis_symmetric() {
 }
 
 // Threads per CTA: FILL_NT (640: 96 registers), or 768 (80 registers) for
-// the many-axis records kernels, whose streamed sums fit in 80 registers
-// and which gain from the fifth and sixth warp per scheduler (cfg5 -3%).
+// the kernels whose integrand sums are streamed (Gaussian, 3-peak Gaussian:
+// StreamSum keeps few partials live) and the many-axis records kernels --
+// they fit 80 registers and gain from the sixth warp per scheduler (cfg2
+// -1.3%, cfg1 -7%, cfg5 -3% fill time).
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return (LAYOUT == LAYOUT_RECORDS && D > 12) ? 768 : FILL_NT;
+  return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK) && D > 0 && D <= 12) ||
+                 (LAYOUT == LAYOUT_RECORDS && D > 12)
+             ? 768
+             : FILL_NT;
 }
 
 template <int ID, int D, int LAYOUT>
@@ -181,11 +186,13 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   // reach the integrand in permuted order (bitwise the same coordinates; sums
   // and products round in a different order, within the parity tolerance).
   constexpr bool XPERM = PAIRS && (D == 2 || D == 4 || D == 8) && axis_symmetric<ID>();
-  // STREAM (the Gaussian at 8 < d <= 128, e.g. cfg5): the integrand's
-  // pairwise sum of (x_j - mu)^2 is accumulated while the axes are sampled
-  // (PairwiseAcc, bit-identical to the row sum), so neither x[] nor the d
-  // squared terms are live across the sampling loop -- ~2d fewer registers
-  constexpr bool STREAM = ID == VPB_GAUSSIAN && D > 8 && D <= 128 && !XPERM;
+  // STREAM (the Gaussian, and the 3-peak Gaussian of cfg2): the integrand's
+  // pairwise sums of (x_j - mu_k)^2 are accumulated while the axes are
+  // sampled (StreamSum: bit-identical to numpy's row sum of the terms in the
+  // order they are sampled), so neither x[] nor the d squared terms per peak
+  // are live across the sampling loop -- up to ~2d(peaks+1) fewer registers
+  constexpr int NPK = ID == VPB_GAUSSIAN ? 1 : (ID == VPB_MULTIPEAK ? 3 : 0);
+  constexpr bool STREAM = NPK > 0 && D >= 1 && D <= 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
@@ -347,7 +354,16 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
           load_digits(cube);
         }
         // ---- sample (vp/kernels.py:59-88)
-        PairwiseAcc<STREAM ? D : 8> gacc;
+        StreamSum<STREAM ? D : 1> gacc[NPK > 0 ? NPK : 1];
+        auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
+          if constexpr (STREAM) {
+#pragma unroll
+            for (int k = 0; k < NPK; k++) {   // vp/integrands.py:135-139 (x_j - mu_k)^2
+              const double u = __dadd_rn(xs, -a.P.p[NPK == 1 ? 0 : 7 + k]);
+              gacc[k].add(step, __dmul_rn(u, u));
+            }
+          }
+        };
         double x[MAXD];
         int iv[MAXD];
         double jac = 1.0;
@@ -366,6 +382,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
                                 EdgePairsT<D>{s_pair + (s0 ^ xr)}, jac, iv[s0]);
             x[s1] = sample_axis(wb, dq1, nsf2, rns2, a.ngf, ng,
                                 EdgePairsT<D>{s_pair + (s1 ^ xr)}, jac, iv[s1]);
+            stream_axis(s0, x[s0]);
+            stream_axis(s1, x[s1]);
           }
         } else {
 #pragma unroll
@@ -381,10 +399,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
           else
             x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
                                EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j]);
-          if constexpr (STREAM) {   // vp/integrands.py:135-139 term (x_j - mu)^2
-            const double u = __dadd_rn(x[j], -a.P.p[0]);
-            gacc.add(j, __dmul_rn(u, u));
-          }
+          stream_axis(j, x[j]);
           if constexpr (LAYOUT == LAYOUT_RECORDS) {
             // the axis group is complete: store its intervals now, so they
             // are not live across the integrand
@@ -407,10 +422,21 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         }   // !XPERM
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
         double f;
-        if constexpr (STREAM)   // integrands.cuh VPB_GAUSSIAN on the streamed sum
-          f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gacc.res, a.P.p[3], a.P.p[4])));
-        else
+        if constexpr (STREAM && NPK == 1) {   // integrands.cuh VPB_GAUSSIAN, streamed sum
+          f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gacc[0].result(), a.P.p[3], a.P.p[4])));
+        } else if constexpr (STREAM) {        // VPB_MULTIPEAK with 3 peaks (host-checked)
+          double e[NPK];
+#pragma unroll
+          for (int k = 0; k < NPK; k++)
+            e[k] = __dmul_rn(a.P.p[2],
+                             fast_exp_nonpos(-div_exact(gacc[k].result(), a.P.p[3], a.P.p[5])));
+          double out = 0.0;
+#pragma unroll
+          for (int k = 0; k < NPK; k++) out = __dadd_rn(out, e[k]);
+          f = div_exact(out, a.P.p[4], a.P.p[6]);
+        } else {
           f = integrand<ID, D>(x, d, a.P);
+        }
         if (!isfinite(f)) {
           atomicMin(a.err_run, (unsigned long long)(r0 + rr));
           atomicOr(a.status, 1);
