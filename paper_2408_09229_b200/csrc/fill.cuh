@@ -42,7 +42,10 @@ namespace vpb {
 #ifndef VPB_FILL_RPT
 #define VPB_FILL_RPT 16
 #endif
-constexpr int FILL_NT = VPB_FILL_NT;    // threads per CTA (one CTA per SM)
+constexpr int FILL_NT = VPB_FILL_NT;
+#ifndef VPB_STREAM_NT
+#define VPB_STREAM_NT 768   // threads of the streamed-sum and many-axis records kernels
+#endif    // threads per CTA (one CTA per SM)
 constexpr int FILL_RPT = VPB_FILL_RPT;  // consecutive runs per lane per tile
 constexpr int FILL_TILE = 32 * FILL_RPT;   // runs per warp tile
 constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
@@ -161,7 +164,7 @@ template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
   return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK) && D > 0 && D <= 12) ||
                  (LAYOUT == LAYOUT_RECORDS && D > 12)
-             ? 768
+             ? VPB_STREAM_NT
              : FILL_NT;
 }
 
