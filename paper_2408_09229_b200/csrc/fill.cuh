@@ -162,7 +162,8 @@ __host__ __device__ constexpr bool axis_symmetric() {
 // -1.3%, cfg1 -7%, cfg5 -3% fill time).
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK) && D > 0 && D <= 12) ||
+  return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
+           ID == VPB_GENZ_PRODUCTPEAK) && D > 0 && D <= 12) ||
                  (LAYOUT == LAYOUT_RECORDS && D > 12)
              ? VPB_STREAM_NT
              : FILL_NT;
@@ -196,6 +197,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   // are live across the sampling loop -- up to ~2d(peaks+1) fewer registers
   constexpr int NPK = ID == VPB_GAUSSIAN ? 1 : (ID == VPB_MULTIPEAK ? 3 : 0);
   constexpr bool STREAM = NPK > 0 && D >= 1 && D <= 128;
+  // the Genz functors (cfg4) reduce left to right over the axes in order
+  // (never XPERM-permuted): a running dot product / product is the streamed
+  // form, bit-identical to integrands.cuh
+  constexpr bool GSTREAM = (ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK) && D > 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
@@ -358,7 +363,14 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         }
         // ---- sample (vp/kernels.py:59-88)
         StreamSum<STREAM ? D : 1> gacc[NPK > 0 ? NPK : 1];
+        double gz = ID == VPB_GENZ_PRODUCTPEAK ? 1.0 : 0.0;   // GSTREAM running value
         auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
+          if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {   // s += x_j a_j
+            gz = __dadd_rn(gz, __dmul_rn(xs, a.P.p[1 + step]));
+          } else if constexpr (GSTREAM) {   // prod *= 1 / (a_j^-2 + (x_j - u_j)^2)
+            const double u = __dadd_rn(xs, -a.P.p[D + step]);
+            gz = __dmul_rn(gz, __drcp_rn(__dadd_rn(a.P.p[step], __dmul_rn(u, u))));
+          }
           if constexpr (STREAM) {
 #pragma unroll
             for (int k = 0; k < NPK; k++) {   // vp/integrands.py:135-139 (x_j - mu_k)^2
@@ -437,6 +449,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
 #pragma unroll
           for (int k = 0; k < NPK; k++) out = __dadd_rn(out, e[k]);
           f = div_exact(out, a.P.p[4], a.P.p[6]);
+        } else if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {
+          f = cos(__dadd_rn(a.P.p[0], gz));   // cos(2 pi u_1 + a.x)
+        } else if constexpr (GSTREAM) {
+          f = gz;
         } else {
           f = integrand<ID, D>(x, d, a.P);
         }
