@@ -43,6 +43,9 @@ namespace vpb {
 #define VPB_FILL_RPT 16
 #endif
 constexpr int FILL_NT = VPB_FILL_NT;
+#ifndef VPB_ALL_NT768
+#define VPB_ALL_NT768 0
+#endif
 #ifndef VPB_STREAM_NT
 #define VPB_STREAM_NT 768   // threads of the streamed-sum and many-axis records kernels
 #endif    // threads per CTA (one CTA per SM)
@@ -159,11 +162,13 @@ __host__ __device__ constexpr bool axis_symmetric() {
 // the kernels whose integrand sums are streamed (Gaussian, 3-peak Gaussian:
 // StreamSum keeps few partials live) and the many-axis records kernels --
 // they fit 80 registers and gain from the sixth warp per scheduler (cfg2
-// -1.3%, cfg1 -7%, cfg5 -3% fill time).
+// -1.3%, cfg1 -7%, cfg4 -5..7%, cfg5 -3%, cfg3 ridge -1% fill time; the d=10
+// registry functors spill at 80 registers and keep 640).
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
   return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
-           ID == VPB_GENZ_PRODUCTPEAK) && D > 0 && D <= 12) ||
+           ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) && D > 0 &&
+          D <= 12) ||
                  (LAYOUT == LAYOUT_RECORDS && D > 12)
              ? VPB_STREAM_NT
              : FILL_NT;
