@@ -20,8 +20,8 @@ Contract (BASELINE.json metric; one JSON line from rank 0):
   time; e2e = the same metric through the public host-buffer call
   (vpb_iteration_host: H2D of the map, D2H of estimate/variance/evals/map).
 * roofline: the fused fill kernel against the FP64 pipe (measured DFMA rate
-  on this GPU), algorithmic FP64 ops per evaluation from SURVEY.md §8(d)
-  with the transcendental costs of bench_costs below.
+  on this GPU); work per evaluation in FP64-pipe instruction equivalents by
+  SURVEY.md §8(d)'s formula with the SASS-measured costs in COST below.
 * cpu_baseline: the C oracle port (oracle/) on this host's cores, rank 0,
   N=1, bounded sample.  --impl reference: the same oracle as the reference
   arm (the reference is Python and cannot travel to the GPU box).
@@ -42,26 +42,36 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # --------------------------------------------------------------- workloads --
-# FP64 ops per evaluation (add/sub/mul/div = 1) and
-# transcendental calls per evaluation.  exp is costed at the FP64-pipe
-# instruction count of the device exp (devmath.cuh fast_exp: 2 clamps,
-# 4 reduction, 14 polynomial, 2 scaling = 22), cos at the libdevice cos
-# instruction count measured from SASS (~40).
-TRANSCENDENTAL_COST = {"exp": 22, "cos": 40}
+# Roofline work per evaluation in FP64-pipe instruction equivalents, the
+# formula of SURVEY.md §8(d): add/sub/mul count + c_div * divisions +
+# c_exp * exps + c_cos * coss, with the costs read from the SASS of the
+# device code (frozen here): an exactly rounded division is 3 FP64-pipe
+# instructions (Markstein: DMUL + 2 DFMA, devmath.cuh div_exact), the device
+# exp 18 (fast_exp_nonpos: 1 clamp + Cody-Waite 4 + degree-11 Horner 11 +
+# 2 scaling), libdevice cos 16.  `flops` is SURVEY §8(d)'s FLOP count
+# (add/sub/mul/div = 1) and `div` the divisions in it.  cfg3: the ridge
+# centres c_i = i/999 are constants of the integrand, staged once per CTA
+# (integrands.cuh ridge_window), so the per-term division is not per-
+# evaluation work: 3227 - 632 FLOP, 8 sampling divisions.
+COST = {"div": 3, "exp": 18, "cos": 16}
 CONFIGS = {
-    "cfg1": dict(integrand="gaussian", dims=4, n_eval=10**6, ng=1000, flops=65, exp=1),
-    "cfg2": dict(integrand="multipeak8", dims=8, n_eval=10**8, ng=1024, flops=177, exp=3),
-    "cfg3": dict(integrand="ridge", dims=4, n_eval=10**8, ng=1024, flops=3227, exp=632),
-    "cfg4a": dict(integrand="genz_oscillatory6", dims=6, n_eval=10**9, ng=1024, flops=88, cos=1),
-    "cfg4b": dict(integrand="genz_productpeak6", dims=6, n_eval=10**9, ng=1024, flops=105),
-    "cfg5": dict(integrand="gaussian20", dims=20, n_eval=4 * 10**9, ng=1024, flops=305, exp=1),
+    "cfg1": dict(integrand="gaussian", dims=4, n_eval=10**6, ng=1000, flops=65, div=9, exp=1),
+    "cfg2": dict(integrand="multipeak8", dims=8, n_eval=10**8, ng=1024, flops=177, div=20, exp=3),
+    "cfg3": dict(integrand="ridge", dims=4, n_eval=10**8, ng=1024, flops=2595, div=8, exp=633),
+    "cfg4a": dict(integrand="genz_oscillatory6", dims=6, n_eval=10**9, ng=1024, flops=88, div=12,
+                  cos=1),
+    "cfg4b": dict(integrand="genz_productpeak6", dims=6, n_eval=10**9, ng=1024, flops=105, div=18),
+    "cfg5": dict(integrand="gaussian20", dims=20, n_eval=4 * 10**9, ng=1024, flops=305, div=41,
+                 exp=1),
 }
 METRIC = "integrand evals/sec per iteration (1/2/4/8 B200) + % FP64 roofline vs host CPU ref"
 UNIT = "evals/s"
 
 
 def fp64_ops_per_eval(cfg) -> float:
-    return cfg["flops"] + sum(cfg.get(k, 0) * v for k, v in TRANSCENDENTAL_COST.items())
+    """add/sub/mul + c_div*div + c_exp*exp + c_cos*cos."""
+    return (cfg["flops"] - cfg.get("div", 0) + COST["div"] * cfg.get("div", 0)
+            + COST["exp"] * cfg.get("exp", 0) + COST["cos"] * cfg.get("cos", 0))
 
 
 # ------------------------------------------------------------------ clocks --
@@ -295,8 +305,10 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
                          "peak": peak_ops / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak_ops, "traffic": traffic,
                          "kernel": "vpb::fill_kernel (fused Philox->map->integrand->histograms)",
-                         "convention": "FP64 pipe ops/s, add/mul/fma = 1 op; peak = measured "
-                                       "DFMA rate on this GPU (vpb_fp64_peak)",
+                         "convention": "FP64-pipe instruction equivalents per SURVEY 8(d): "
+                                       "add/sub/mul=1, exact div=3, exp=18, cos=16 (SASS "
+                                       "counts); peak = measured DFMA rate on this GPU "
+                                       "(vpb_fp64_peak)",
                          "ops_per_eval": ops, "fill_kernel_ms_per_step": fill_ms_max / steps,
                          "fill_share_of_step": fill_ms_max / t_max},
             "cpu_baseline": cpu,

@@ -756,18 +756,20 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // shared-histogram candidates in order: (pairs, padded stride), (pairs,
   // stride d), (edge rows, padded), (edge rows, stride d)
   c->hs = hist_stride(c->dims);
+  // the ridge kernels stage the centre table (specialised kernels only)
+  const int rc_n = (c->id == VPB_RIDGE && specialisable(c)) ? (int)c->P.p[0] : 0;
   bool fits = false;
   for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
     const bool pr = pass < 2 && c->pairs;
     if (pass < 2 && !c->pairs) continue;
     const int hs = (pass & 1) ? c->dims : hist_stride(c->dims);
-    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, pr, hs);
+    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, pr, hs, rc_n);
     if (b <= (size_t)optin) { fits = true; c->pairs = pr; c->hs = hs; c->smem = b; }
   }
   if (!fits) {
     c->smem_hist = false;
     c->pairs = false;
-    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0, 0);
+    c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0, 0, rc_n);
   }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
@@ -784,7 +786,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // a records-layout fill with d >= 12 histograms its first REC_K0 axes in
   // the shared memory left next to the edges (fill.cuh K0)
   if (layout == LAYOUT_RECORDS && c->dims >= 12) {
-    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, 0, REC_K0);
+    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, 0, REC_K0, rc_n);
     if (b > (size_t)optin) return bail(fail(VPB_ERR_UNSUPPORTED, "records layout does not fit"));
     c->rec_k0 = REC_K0;
     c->hs = REC_K0;

@@ -126,13 +126,15 @@ __host__ __device__ inline int hist_stride(int dims) {
 
 // shared-memory layout helper (bytes)
 __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
-                                                  int smem_hist, int pairs, int hs) {
+                                                  int smem_hist, int pairs, int hs,
+                                                  int ridge_centres = 0) {
   size_t b = 0;
   if (pairs) b += (size_t)dims * ng * 2 * sizeof(double);              // (E[i], dx[i])
   else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
   if (smem_hist) b += (size_t)hs * ng * (sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
+  b += (size_t)ridge_centres * sizeof(double);                          // ridge c_i
   b += 16;                                                              // block flags
   return b;
 }
@@ -229,6 +231,11 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   const bool dq_tab = a.n_strat <= DQ_TABLE_MAX;
   double *s_dq = reinterpret_cast<double *>(smem_raw + off);
   off += (dq_tab ? (size_t)a.n_strat : 0) * sizeof(double);
+  // ridge: centres c_i = RN(i/(n-1)) (integrands.cuh ridge_window)
+  constexpr bool RTAB = ID == VPB_RIDGE && D > 0;
+  double *s_ctab = reinterpret_cast<double *>(smem_raw + off);
+  const int n_cent = RTAB ? (int)a.P.p[0] : 0;
+  off += (size_t)n_cent * sizeof(double);
   const int dbits = a.dig_bits;                 // bits per packed digit (!DQ_REG)
   const uint64_t dmask = (1ull << dbits) - 1;
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
@@ -247,6 +254,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
     for (int i = tid; i < hs * ng; i += NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
   if (dq_tab)
     for (int i = tid; i < a.n_strat; i += NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
+  if constexpr (RTAB) {
+    const double spacing = (double)n_cent - 1.0, rsp = 1.0 / spacing;
+    for (int i = tid; i < n_cent; i += NT) s_ctab[i] = div_exact((double)i, spacing, rsp);
+  }
 
   if (tid == 0) s_flag[0] = *a.status;   // an earlier iteration failed: nothing to fill
   const Sched S = *a.sched;
@@ -459,7 +470,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         } else if constexpr (GSTREAM) {
           f = gz;
         } else {
-          f = integrand<ID, D>(x, d, a.P);
+          f = integrand<ID, D>(x, d, a.P, RTAB ? s_ctab : nullptr);
         }
         if (!isfinite(f)) {
           atomicMin(a.err_run, (unsigned long long)(r0 + rr));

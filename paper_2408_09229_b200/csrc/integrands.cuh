@@ -69,8 +69,33 @@ __device__ __forceinline__ double erfinv_ref(double y) {
   return copysign(z, y);
 }
 
+// Ridge window sum (vp/integrands.py:154-182) over the centres c_i = i/(n-1)
+// for i in [lo, hi]: sum_i exp(-400 (c_i - mu)^2).  `ctab` (optional) holds
+// RN(i/(n-1)) precomputed (the fill kernel stages it in shared memory: the
+// same bits as the division, three FP64 ops cheaper per term); the
+// exponent lies in [-46.1, 0] inside the window, so the unclamped exp core
+// is exact to the clamped one.
+__device__ __forceinline__ double ridge_window(double mu, int lo, int hi, double spacing,
+                                               const double *ctab) {
+  double acc = 0.0;
+  if (ctab) {
+    for (int i = lo; i <= hi; i++) {
+      const double dc = __dadd_rn(ctab[i], -mu);
+      acc = __dadd_rn(acc, fast_exp_core(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
+    }
+  } else {
+    const double rsp = 1.0 / spacing;
+    for (int i = lo; i <= hi; i++) {
+      const double dc = __dadd_rn(div_exact((double)i, spacing, rsp), -mu);
+      acc = __dadd_rn(acc, fast_exp_nonpos(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
+    }
+  }
+  return acc;
+}
+
 template <int ID, int D>
-__device__ __forceinline__ double integrand(const double *x, int d, const IParams &P) {
+__device__ __forceinline__ double integrand(const double *x, int d, const IParams &P,
+                                            const double *ctab = nullptr) {
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   if constexpr (ID == VPB_GAUSSIAN) {
     // norm * exp(-sum((x-mu)^2) / (2 sigma^2))           vp/integrands.py:135-139
@@ -151,12 +176,7 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     int hi = (int)floor(__dmul_rn(__dadd_rn(mu, P.p[2]), spacing));
     lo = lo < 0 ? 0 : lo;
     hi = hi > n_cent - 1 ? n_cent - 1 : hi;
-    const double rsp = 1.0 / spacing;
-    double acc = 0.0;
-    for (int i = lo; i <= hi; i++) {
-      const double dc = __dadd_rn(div_exact((double)i, spacing, rsp), -mu);
-      acc = __dadd_rn(acc, fast_exp_nonpos(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
-    }
+    const double acc = ridge_window(mu, lo, hi, spacing, ctab);
     // q0 = s2 - s1^2/4 >= 0 up to rounding: the general exp
     return __dmul_rn(__dmul_rn(P.p[1], fast_exp(__dmul_rn(-100.0, q0))), acc);
   } else if constexpr (ID == VPB_GENZ_OSCILLATORY) {
