@@ -414,15 +414,19 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
       a.tile_lo = ch * tpc;
       a.tile_hi = (ch + 1) * tpc;
       CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
-      for (int g = 0; g < c->n_groups; g++) {
-        const int jn = std::min(8, c->dims - c->rec_k0 - 8 * g);
-        const size_t goff = (size_t)g * c->rec_B * c->ng * 8;
-        const size_t sm = hist_records_smem(c->ng);
+      // the full 8-axis groups in one launch (grid.y = groups), then a partial
+      const int n_rec = c->dims - c->rec_k0, n_full = n_rec / 8, jn_last = n_rec % 8;
+      const size_t sm = hist_records_smem(c->ng);
+      for (int part = 0; part < 2; part++) {
+        const int g0 = part ? n_full : 0, ng_l = part ? (jn_last ? 1 : 0) : n_full;
+        const int jn = part ? jn_last : 8;
+        if (ng_l == 0) continue;
+        const dim3 grid((unsigned)c->rec_B, (unsigned)ng_l);
 #define VPB_HR(J)                                                                           \
   case J:                                                                                   \
-    hist_records_kernel<J><<<c->rec_B, HR_NT, sm, c->st>>>(                                 \
-        c->rec_iv, c->rec_w2, c->rec_ch, a.tile_lo, c->sched, c->ng, g, c->hw_rec + goff,   \
-        c->hc_rec + goff, ch == 0, c->status);                                              \
+    hist_records_kernel<J><<<grid, HR_NT, sm, c->st>>>(                                     \
+        c->rec_iv, c->rec_w2, c->rec_ch, a.tile_lo, c->sched, c->ng, g0, c->hw_rec,         \
+        c->hc_rec, ch == 0, c->status);                                                     \
     break;
         switch (jn) {
           VPB_HR(1) VPB_HR(2) VPB_HR(3) VPB_HR(4) VPB_HR(5) VPB_HR(6) VPB_HR(7) VPB_HR(8)
@@ -821,7 +825,9 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&hr_per_sm, hist_records_kernel<8>, HR_NT,
                                                       hsm) != cudaSuccess || hr_per_sm < 1)
       return bail(fail(VPB_ERR_CUDA, "hist_records kernel cannot be resident"));
-    c->rec_B = std::max(1, (sms * hr_per_sm + c->n_groups - 1) / c->n_groups);
+    // CTAs per group: the full groups share one launch at hr_per_sm CTAs per SM
+    const int n_full = std::max(1, (c->dims - c->rec_k0) / 8);
+    c->rec_B = std::max(1, (sms * hr_per_sm + n_full - 1) / n_full);
     A(c->rec_iv, (size_t)c->n_groups * c->rec_ch * 8);
     A(c->rec_w2, (size_t)c->rec_ch);
     A(c->hw_rec, (size_t)c->n_groups * c->rec_B * c->ng * 8);
@@ -1038,7 +1044,8 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   if (n_chunks) *n_chunks = c->records ? c->n_chunks : 0;
   // plan_scan, plan_offsets, fill | chunks x (fill + groups), fixup, histogram
   // reduce, cube_terms, results_leaf, results_tree, alloc, refine, step, mark
-  const int fill = c->records ? c->n_chunks * (1 + c->n_groups) : 1;
+  const int n_rec = c->dims - c->rec_k0;
+  const int fill = c->records ? c->n_chunks * (1 + (n_rec >= 8) + (n_rec % 8 != 0)) : 1;
   if (launches) *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 2;
   return VPB_OK;
 }

@@ -27,12 +27,14 @@ __host__ __device__ inline size_t hist_records_smem(int ng) {
   return (size_t)ng * 8 * (sizeof(double) + sizeof(unsigned));
 }
 
-// grid (B, n_groups); group g covers axes [8g, min(8g+8, dims)); JN = axes in
-// the group (compile time; the last group may be partial)
+// grid (B, G): blockIdx.y = group g0 + y, covering record axes [8g, 8g + JN);
+// JN = axes per group (compile time: the full groups of a chunk run in one
+// launch, two CTAs per SM; a partial last group gets its own launch).  Group
+// g's B slices start at hw_rec / hc_rec + g * B * ng * 8.
 template <int JN>
 __global__ void __launch_bounds__(HR_NT, 2)
     hist_records_kernel(const unsigned short *rec_iv, const double *rec_w2, long long rec_ch,
-                        long long tile_lo, const Sched *sched, int ng, int g,
+                        long long tile_lo, const Sched *sched, int ng, int g0,
                         double *hw_rec, unsigned *hc_rec, int first, const int *status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double *s_hw = reinterpret_cast<double *>(smem_raw);
@@ -42,7 +44,8 @@ __global__ void __launch_bounds__(HR_NT, 2)
   const long long run0 = tile_lo * FILL_TILE;              // chunk start relative to lo
   const long long n = max(0ll, min(rec_ch, S.hi - S.lo - run0));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const size_t slice = (size_t)blockIdx.x * ng * 8;
+  const int g = g0 + (int)blockIdx.y;
+  const size_t slice = ((size_t)g * gridDim.x + blockIdx.x) * ng * 8;
   double *gw = hw_rec + slice;
   unsigned *gc = hc_rec + slice;
   if (n == 0) {                                             // block-uniform
