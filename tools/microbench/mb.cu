@@ -73,6 +73,15 @@ __global__ void gredk(double* bins, int iters, int nb){
     for(int u=0;u<4;u++){ x=x*1664525u+1013904223u; unsigned b=(x>>8)%nb; atomicAdd(&bins[b],1.0);} 
   }
 }
+// global f64 red into a per-CTA private slice of nb bins (L2-resident)
+__global__ void gredslk(double* bins, int iters, int nb){
+  double* mine=bins+(size_t)blockIdx.x*nb;
+  unsigned x=threadIdx.x*2654435761u+blockIdx.x*97u+1;
+  for(int i=0;i<iters;i++){
+    #pragma unroll 4
+    for(int u=0;u<4;u++){ x=x*1664525u+1013904223u; unsigned b=(x>>8)%nb; atomicAdd(&mine[b],1.0);}
+  }
+}
 // exp cost
 __global__ void expk(double* out, int iters){
   double a=-threadIdx.x*1e-3, s=0;
@@ -111,6 +120,13 @@ int main(){
   int gnb[3]={20480, 4096, 1<<20};
   for(int q=0;q<3;q++){ char nm[64]; sprintf(nm,"REDG f64 nb=%d",gnb[q]);
     cudaEventRecord(e0); gredk<<<blocks,threads>>>(bins,it/20,gnb[q]); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep(nm,(double)blocks*threads*(it/20)*4);
+  }
+  double* sl; CK(cudaMalloc(&sl, (size_t)8*SM*8192)); cudaMemset(sl,0,(size_t)8*SM*8192);
+  { char nm[64]; sprintf(nm,"REDG f64 per-CTA slice nb=8192");
+    cudaEventRecord(e0); gredslk<<<SM,768>>>(sl,it/20,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep(nm,(double)SM*768*(it/20)*4);
+    cudaFuncSetAttribute(smemk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+    cudaEventRecord(e0); smemk<1><<<SM,768,8192*8>>>(out,it/20,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep("ATOMS f64 CAS 768thr 1CTA/SM nb=8192",(double)SM*768*(it/20)*4);
+    cudaEventRecord(e0); smemk<0><<<SM,768,8192*8>>>(out,it/20,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep("ATOMS u32 768thr 1CTA/SM nb=8192",(double)SM*768*(it/20)*4);
   }
   }
   return 0;
