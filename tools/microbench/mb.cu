@@ -82,6 +82,25 @@ __global__ void gredslk(double* bins, int iters, int nb){
     for(int u=0;u<4;u++){ x=x*1664525u+1013904223u; unsigned b=(x>>8)%nb; atomicAdd(&mine[b],1.0);}
   }
 }
+// mixed: of every 8 f64 updates, R go to a per-CTA global slice (REDG), the
+// rest to shared memory (CAS.SPIN) -- do the two paths add up?
+template<int R> __global__ void mixk(double* gbins, double* out, int iters, int nb){
+  extern __shared__ double sh[];
+  double* mine=gbins+(size_t)blockIdx.x*nb;
+  for(int i=threadIdx.x;i<nb;i+=blockDim.x){sh[i]=0;}
+  __syncthreads();
+  unsigned x=threadIdx.x*2654435761u+blockIdx.x*97u+1;
+  for(int i=0;i<iters;i++){
+    #pragma unroll
+    for(int u=0;u<8;u++){
+      x=x*1664525u+1013904223u; unsigned b=(x>>8)%nb;
+      if(u<R) atomicAdd(&mine[b],1.0); else atomicAdd(&sh[b],1.0);
+    }
+  }
+  __syncthreads();
+  double s=0; for(int i=threadIdx.x;i<nb;i+=blockDim.x) s+=sh[i];
+  out[blockIdx.x*blockDim.x+threadIdx.x]=s;
+}
 // exp cost
 __global__ void expk(double* out, int iters){
   double a=-threadIdx.x*1e-3, s=0;
@@ -127,6 +146,10 @@ int main(){
     cudaFuncSetAttribute(smemk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
     cudaEventRecord(e0); smemk<1><<<SM,768,8192*8>>>(out,it/20,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep("ATOMS f64 CAS 768thr 1CTA/SM nb=8192",(double)SM*768*(it/20)*4);
     cudaEventRecord(e0); smemk<0><<<SM,768,8192*8>>>(out,it/20,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); rep("ATOMS u32 768thr 1CTA/SM nb=8192",(double)SM*768*(it/20)*4);
+#define MIX(R) cudaFuncSetAttribute(mixk<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); \
+    cudaEventRecord(e0); mixk<R><<<SM,768,8192*8>>>(sl,out,it/40,8192); cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); \
+    sprintf(nm,"mix %d/8 REDG + rest CAS, 768thr",R); rep(nm,(double)SM*768*(it/40)*8);
+    MIX(0) MIX(1) MIX(2) MIX(3) MIX(4)
   }
   }
   return 0;
