@@ -394,10 +394,13 @@ int join_side(vpb_ctx *c) {
 
 // join_after: join the side stream before returning (host entry points and
 // the multi-GPU all-reduce); the iteration body defers it to the update.
+// zero_cubes: clear s1/s2 first.  Not needed when this context's shard is the
+// whole plan (world 1): every cube has >= 1 run and the fill / fixup assign
+// (never accumulate) each cube's sums exactly once.
 int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr,
-                 bool defer_join = false) {
+                 bool defer_join = false, bool zero_cubes = true) {
   const size_t m = (size_t)c->dims * c->ng;
-  CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
+  if (zero_cubes) CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
   if (!c->smem_hist && !c->records) {
     CK(cudaMemsetAsync(c->hw_glob, 0, sizeof(double) * m, c->st));
     CK(cudaMemsetAsync(c->hc_glob, 0, sizeof(unsigned long long) * m, c->st));
@@ -508,7 +511,7 @@ int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
   CK(rec_event(c, E[0]));
   TRY(enqueue_plan(c, 1, nullptr));
   CK(rec_event(c, E[1]));
-  TRY(enqueue_fill(c, false, E[2], E[3], /*defer_join=*/true));
+  TRY(enqueue_fill(c, false, E[2], E[3], /*defer_join=*/true, /*zero_cubes=*/c->world > 1));
   CK(rec_event(c, E[4]));
   TRY(enqueue_update(c, 1));
   CK(rec_event(c, E[5]));
@@ -1211,7 +1214,7 @@ int vpb_fill(vpb_ctx *c, int64_t run_base) {
   TRY(setdev(c));
   CK(cudaMemcpyAsync(c->explicit_rb, &run_base, sizeof(long long), cudaMemcpyHostToDevice, c->st));
   TRY(enqueue_plan(c, 0, c->explicit_rb));
-  TRY(enqueue_fill(c, true));
+  TRY(enqueue_fill(c, true, nullptr, nullptr, false, c->world > 1));
   CK(cudaStreamSynchronize(c->st));
   int status = 0;
   CK(cudaMemcpy(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost));
