@@ -488,7 +488,8 @@ int enqueue_update(vpb_ctx *c, int record) {
       c->pwterms, c->n_cubes, pd, c->pwvals, c->status);
   const size_t tsm = pw_tree_smem(pd);
   results_tree_kernel<<<1, 1024, tsm, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
-                                               c->h_var, c->sched, c->status, record, tsm > 0);
+                                               c->h_var, c->sched, c->status, record,
+                                               pw_tree_flags(pd));
   alloc_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->dp, c->n_cubes, c->beta,
                                                        (double)c->n_eval, c->uniform_nh, c->sc, 0,
                                                        c->n_h, c->bsum, c->status);
@@ -1460,7 +1461,7 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   CK(cudaFuncSetAttribute(results_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)PW_TREE_SMEM_MAX));
   results_tree_kernel<<<1, 1024, tsm>>>(pw.dev(), vals.p, n, V, sc.p, he.p, hv.p, sch.p, st.p, 0,
-                                        tsm > 0);
+                                        pw_tree_flags(pw.dev()));
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   Scalars s;

@@ -121,35 +121,66 @@ __global__ void array_leaf_kernel(const double *a, PwPlanDev pw, double *vals) {
 }
 
 // Inner nodes of the pairwise tree, by height, one CTA; three sums at once.
-// When the whole tree fits (`sv` != nullptr: dynamic shared memory of
-// 3*(L+I) doubles) the leaves are staged there and every level combines in
-// shared memory; otherwise the levels combine in `vals` (global).
-__device__ void pw_tree_combine(PwPlanDev pw, double *vals, double *sv = nullptr) {
+// Shared-memory staging (`flags`, from pw_tree_flags): bit 0 -- the leaf
+// values are copied into `sm` and every level combines there; bit 1 -- the
+// node tables (children, level starts) are copied too, so the H dependent
+// levels read no global memory (after an L2 flush each level's index loads
+// were a DRAM round trip).  Without staging the levels combine in `vals`.
+__device__ void pw_tree_combine(PwPlanDev pw, double *vals, unsigned char *sm = nullptr,
+                                int flags = 0) {
   double *v = vals;
-  if (sv) {
+  const int *nl = pw.node_l, *nr = pw.node_r, *ls = pw.level_start;
+  unsigned char *p = sm;
+  if (flags & 1) {
+    double *sv = reinterpret_cast<double *>(p);
     for (int i = threadIdx.x; i < 3 * pw.L; i += blockDim.x) sv[i] = vals[i];
-    __syncthreads();
     v = sv;
+    p += sizeof(double) * 3 * (size_t)(pw.L + pw.I);
   }
+  if (flags & 2) {
+    int *si = reinterpret_cast<int *>(p);
+    for (int i = threadIdx.x; i < pw.I; i += blockDim.x) {
+      si[i] = pw.node_l[i];
+      si[pw.I + i] = pw.node_r[i];
+    }
+    for (int i = threadIdx.x; i <= pw.H; i += blockDim.x) si[2 * pw.I + i] = pw.level_start[i];
+    nl = si;
+    nr = si + pw.I;
+    ls = si + 2 * pw.I;
+  }
+  if (flags) __syncthreads();
   for (int h = 0; h < pw.H; h++) {
-    for (int i = pw.level_start[h] + threadIdx.x; i < pw.level_start[h + 1]; i += blockDim.x) {
-      const int l = pw.node_l[i], r = pw.node_r[i], me = pw.L + i;
+    for (int i = ls[h] + threadIdx.x; i < ls[h + 1]; i += blockDim.x) {
+      const int l = nl[i], r = nr[i], me = pw.L + i;
 #pragma unroll
       for (int c = 0; c < 3; c++) v[3 * me + c] = __dadd_rn(v[3 * l + c], v[3 * r + c]);
     }
     __syncthreads();
   }
-  if (sv && threadIdx.x < 3) {   // the root, for the caller
+  if ((flags & 1) && threadIdx.x < 3) {   // the root, for the caller
     const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
-    vals[3 * root + threadIdx.x] = sv[3 * root + threadIdx.x];
+    vals[3 * root + threadIdx.x] = v[3 * root + threadIdx.x];
   }
   __syncthreads();
 }
 
-constexpr size_t PW_TREE_SMEM_MAX = 200 * 1024;
+constexpr size_t PW_TREE_SMEM_MAX = 220 * 1024;
+inline size_t pw_tree_vals_bytes(const PwPlanDev &pw) {
+  return sizeof(double) * 3 * (size_t)(pw.L + pw.I);
+}
+inline size_t pw_tree_idx_bytes(const PwPlanDev &pw) {
+  return sizeof(int) * (2 * (size_t)pw.I + pw.H + 1);
+}
+// staging flags for pw_tree_combine: values and tables if both fit, else the
+// tables alone
+inline int pw_tree_flags(const PwPlanDev &pw) {
+  const size_t vb = pw_tree_vals_bytes(pw), ib = pw_tree_idx_bytes(pw);
+  if (vb + ib <= PW_TREE_SMEM_MAX) return 3;
+  return ib <= PW_TREE_SMEM_MAX ? 2 : 0;
+}
 inline size_t pw_tree_smem(const PwPlanDev &pw) {
-  const size_t b = sizeof(double) * 3 * (size_t)(pw.L + pw.I);
-  return b <= PW_TREE_SMEM_MAX ? b : 0;
+  const int f = pw_tree_flags(pw);
+  return ((f & 1) ? pw_tree_vals_bytes(pw) : 0) + ((f & 2) ? pw_tree_idx_bytes(pw) : 0);
 }
 
 struct Scalars {
@@ -160,10 +191,10 @@ struct Scalars {
 // Finishes compute_results (vp/strat.py:205-207) and records the history.
 __global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, double V,
                                     Scalars *sc, double *hist_est, double *hist_var,
-                                    Sched *sched, const int *status, int record, int use_smem) {
-  extern __shared__ __align__(16) double tree_sm[];
+                                    Sched *sched, const int *status, int record, int flags) {
+  extern __shared__ __align__(16) unsigned char tree_sm[];
   if (*status & 1) return;
-  pw_tree_combine(pw, vals, use_smem ? tree_sm : nullptr);
+  pw_tree_combine(pw, vals, tree_sm, flags);
   if (threadIdx.x == 0) {
     const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
     const double sm = vals[3 * root], st = vals[3 * root + 1], sp = vals[3 * root + 2];
@@ -235,32 +266,49 @@ __global__ void nh_blocksum_kernel(const long long *n_h, long long n, long long 
   }
 }
 
+// Inclusive int64 scan of one value per thread over a PLAN_NT-thread block:
+// shuffles within warps, one shared step across the 32 warp totals (exact
+// integer sums, so the order is free).  `wsum`: PLAN_NT/32 shared slots; the
+// block must call it uniformly.
+__device__ __forceinline__ long long block_incl_scan(long long v, long long *wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) wsum[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    long long w = lane < PLAN_NT / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    if (lane < PLAN_NT / 32) wsum[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) v += wsum[warp - 1];
+  return v;
+}
+
 // Exclusive scan of the block sums; total; this rank's shard of the run
 // range (vp/executor.py:41-57: the first total % world ranks get +1); run_base
 // bookkeeping (vp/core.py:208) and the evals history.
 __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, int world, int rank,
                                  long long *hist_evals, int record, long long ntiles_cap,
                                  int *status, const long long *explicit_run_base) {
-  __shared__ long long buf[PLAN_NT];
-  __shared__ long long carry;
+  __shared__ long long wsum[PLAN_NT / 32];
   if (*status) return;   // a failed iteration freezes the plan (error reporting)
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
+  long long carry = 0;
   for (long long b0 = 0; b0 < nb; b0 += PLAN_NT) {
     const long long i = b0 + threadIdx.x;
     const long long v = i < nb ? bsum[i] : 0;
-    buf[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = 1; o < PLAN_NT; o <<= 1) {
-      const long long t = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
-      __syncthreads();
-      buf[threadIdx.x] += t;
-      __syncthreads();
-    }
-    if (i < nb) bsum[i] = carry + buf[threadIdx.x] - v;   // exclusive
-    __syncthreads();
-    if (threadIdx.x == 0) carry += buf[PLAN_NT - 1];
-    __syncthreads();
+    const long long inc = block_incl_scan(v, wsum);
+    if (i < nb) bsum[i] = carry + inc - v;   // exclusive
+    carry += wsum[PLAN_NT / 32 - 1];         // this chunk's total (uniform)
+    __syncthreads();                         // wsum reused by the next chunk
   }
   if (threadIdx.x == 0) {
     const long long total = carry;
@@ -286,31 +334,41 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
 __global__ void plan_offsets_kernel(const long long *n_h, long long n, const long long *bpre,
                                     long long *offsets, const Sched *sched, int *tile_cube,
                                     const int *status) {
-  __shared__ long long buf[PLAN_NT];
+  __shared__ long long wsum[PLAN_NT / 32];
   if (status && *status) return;
   const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
   const long long v = h < n ? n_h[h] : 0;
-  buf[threadIdx.x] = v;
-  __syncthreads();
-  for (int o = 1; o < PLAN_NT; o <<= 1) {
-    const long long t = threadIdx.x >= o ? buf[threadIdx.x - o] : 0;
-    __syncthreads();
-    buf[threadIdx.x] += t;
-    __syncthreads();
+  const long long inc = block_incl_scan(v, wsum);
+  const bool valid = h < n;
+  long long t0 = 0, t1 = 0;
+  if (valid) {
+    const long long beg = bpre[blockIdx.x] + inc - v;
+    const long long end = beg + v;
+    offsets[h] = beg;
+    if (h == n - 1) offsets[n] = end;
+    const long long lo = sched->lo, hi = sched->hi;
+    const long long a = beg > lo ? beg : lo, b = end < hi ? end : hi;
+    if (a < b) {
+      // tiles whose first run lies in [a, b)
+      t0 = (a - lo + FILL_TILE - 1) / FILL_TILE;
+      t1 = (b - lo + FILL_TILE - 1) / FILL_TILE;
+      if (b == hi) tile_cube[sched->ntiles] = (int)h;   // sentinel: cube of the last run
+    }
   }
-  if (h >= n) return;
-  const long long beg = bpre[blockIdx.x] + buf[threadIdx.x] - v;
-  const long long end = beg + v;
-  offsets[h] = beg;
-  if (h == n - 1) offsets[n] = end;
-  const long long lo = sched->lo, hi = sched->hi, nt = sched->ntiles;
-  const long long a = beg > lo ? beg : lo, b = end < hi ? end : hi;
-  if (a < b) {
-    // tiles whose first run lies in [a, b)
-    long long t0 = (a - lo + FILL_TILE - 1) / FILL_TILE;
-    const long long t1 = (b - lo + FILL_TILE - 1) / FILL_TILE;
+  // short ranges by their own thread; the big cubes of an adapted plan
+  // (thousands of tiles) by the whole warp, coalesced
+  constexpr long long SHORT = 32;
+  const bool longr = t1 - t0 > SHORT;
+  if (!longr)
     for (long long t = t0; t < t1; t++) tile_cube[t] = (int)h;
-    if (b == hi) tile_cube[nt] = (int)h;   // sentinel: cube of the last run
+  unsigned todo = __ballot_sync(0xffffffffu, longr);
+  const int lane = threadIdx.x & 31;
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const long long u0 = __shfl_sync(0xffffffffu, t0, src), u1 = __shfl_sync(0xffffffffu, t1, src);
+    const int hh = (int)__shfl_sync(0xffffffffu, h, src);
+    for (long long t = u0 + lane; t < u1; t += 32) tile_cube[t] = hh;
   }
 }
 
