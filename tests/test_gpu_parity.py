@@ -240,7 +240,8 @@ def test_integrate_trajectory_matches_oracle(name, dims, n_eval, max_it, ng):
 
 @pytest.mark.parametrize("layout,chunk", [("records", "2048"), ("records", ""), ("global", "")])
 @pytest.mark.parametrize("name,dims,ng,ns,nh", [
-    ("gaussian20", 20, 64, 1, (5000, 5001)),     # 3 axis groups (8, 8, 4)
+    ("gaussian20", 20, 64, 1, (5000, 5001)),     # K0 = 4 axes in the fill + 2 full groups
+    ("gaussian", 13, 48, 2, (2, 40)),            # generic kernel: full group + partial launch
     ("multipeak8", 8, 256, 3, (2, 400)),         # one full group
     ("genz_oscillatory6", 6, 100, 3, (2, 50)),   # one partial group
     ("gaussian", 3, 50, 5, (2, 30)),             # generic (runtime-dims) kernel
