@@ -18,6 +18,10 @@ os.makedirs(dst, exist_ok=True)
 
 
 def json_line(path):
+    try:
+        return json.load(open(path))
+    except ValueError:
+        pass
     for line in open(path):
         line = line.strip()
         if line.startswith("{"):
@@ -52,5 +56,35 @@ if os.path.exists(rep):
                   "launch (ncu --set full, profiles/%s/fill_cfg2_ncu_summary.json; ncu reports "
                   "read in MB and write in KB); the fill is FP64/shared-memory bound, this is "
                   "the map edges + offsets + cube sums that miss L2" % rnd)
+    json.dump(t, open(tp, "w"), indent=1)
+# per-config DRAM traffic of the fill (one launch x launches per step)
+import csv  # noqa: E402
+tp = os.path.join(ROOT, "profiles", "fill_traffic.json")
+t = json.load(open(tp)) if os.path.exists(tp) else {}
+found = False
+for f in sorted(os.listdir(src)):
+    if not (f.startswith("traffic_") and f.endswith(".csv")):
+        continue
+    cfg = f[len("traffic_"):-4]
+    rows = [r for r in csv.reader(l for l in open(os.path.join(src, f)) if l.startswith('"'))]
+    if len(rows) < 2:
+        continue
+    h = rows[0]
+    ix = {n: i for i, n in enumerate(h)}
+    by = {r[ix["Metric Name"]]: float(r[ix["Metric Value"]].replace(",", "")) for r in rows[1:]}
+    per_launch = by.get("dram__bytes_read.sum", 0.0) + by.get("dram__bytes_write.sum", 0.0)
+    bl = os.path.join(dst, "bench_%s.json" % cfg)
+    chunks = 1
+    if os.path.exists(bl):
+        chunks = max(1, int(json.load(open(bl))["config"].get("record_chunks") or 1))
+    t[cfg] = int(per_launch * chunks)
+    found = True
+if found:
+    t["_note"] = ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, ncu) of the fill "
+                  "kernel per step: one launch x the record chunks per iteration (cfg5), "
+                  "captured by tools/gpu_checkpoint.sh into profiles/%s/traffic_*.csv" % rnd)
+    for f in os.listdir(src):
+        if f.startswith("traffic_") and f.endswith(".csv"):
+            shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     json.dump(t, open(tp, "w"), indent=1)
 print(sorted(os.listdir(dst)))
