@@ -4,7 +4,7 @@
 Contract (BASELINE.json metric; one JSON line from rank 0):
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--config cfg2|cfg1|cfg3|cfg4a|cfg4b|cfg5]
+                    [--config cfg2|cfg1|cfg3|cfg4a|cfg4b|cfg5|ra10]
 
 * workload: BASELINE.json configs[1] = cfg2, the 8-D three-peak Gaussian
   (multipeak8), n_eval = 1e8 per iteration per GPU (weak scaling: N GPUs
@@ -63,6 +63,11 @@ CONFIGS = {
     "cfg4b": dict(integrand="genz_productpeak6", dims=6, n_eval=10**9, ng=1024, flops=105, div=18),
     "cfg5": dict(integrand="gaussian20", dims=20, n_eval=4 * 10**9, ng=1024, flops=305, div=41,
                  exp=1),
+    # the paper's own breakdown workload ("def": ng 1024,
+    # 20 iterations; 1e10 evaluations = 5e8 per iteration): Roos & Arnold
+    # 10-D, prod |4 x_j - 2| -- transform 110 (20 div) + integrand 30 +
+    # accumulate 14
+    "ra10": dict(integrand="roos_arnold", dims=10, n_eval=5 * 10**8, ng=1024, flops=154, div=20),
 }
 METRIC = "integrand evals/sec per iteration (1/2/4/8 B200) + % FP64 roofline vs host CPU ref"
 UNIT = "evals/s"
