@@ -8,7 +8,7 @@ timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/$TAG/tests.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/$TAG/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 600 python bench.py > gpurun_out/$TAG/bench_default.json 2> gpurun_out/$TAG/bench_default.err; echo "bench rc=$?"; cat gpurun_out/$TAG/bench_default.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/$TAG/bench_ref.json 2>&1; echo "ref rc=$?"
-for c in cfg1 cfg3 cfg4a cfg4b cfg5; do
+for c in cfg1 cfg3 cfg4a cfg4b cfg5 ra10; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err; echo "bench $c rc=$?"
 done
 bash tools/gpu_profile.sh cfg2 $TAG/p
