@@ -195,7 +195,9 @@ int vpb_fill_host(const int64_t *offsets, int64_t n_cubes, const double *edges, 
                   int64_t *counts, int64_t *err_run, double *err_point, double *err_value);
 /* numpy float64 add.reduce (pairwise) */
 int vpb_pairwise_sum_host(const double *a, int64_t n, double *out);
-/* correctly rounded x**y (the allocation's pow) */
+/* the allocation's d_h**beta on the device, as the fill's update computes it:
+ * numpy's scalar-exponent fast paths (beta 0, 1/2, 1, 2) bit-exact, else
+ * CUDA pow (<= 2 ulp; numpy's pow is host-dependent) */
 int vpb_pow_host(const double *x, int64_t n, double y, double *out);
 /* strat.update_evals_per_cube (vp/strat.py:88-113) */
 int vpb_update_evals_host(const double *d_h, int64_t n, double beta, int64_t n_eval,
