@@ -55,7 +55,10 @@ constexpr int DQ_TABLE_MAX = 2048;             // digit/N table when N <= this
 #ifndef VPB_DQ_REG_MAX
 #define VPB_DQ_REG_MAX 12   // dims up to which RN(digit/N) stays in registers
 #endif
-constexpr int REC_K0 = 4;   // axes kept in shared memory by a records-layout fill (d >= 12)
+#ifndef VPB_REC_K0
+#define VPB_REC_K0 4
+#endif
+constexpr int REC_K0 = VPB_REC_K0;   // axes kept in shared memory by a records-layout fill (d >= 12)
 
 // Per-iteration schedule written by the plan kernels (device memory).
 struct Sched {
