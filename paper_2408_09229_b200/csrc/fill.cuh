@@ -169,9 +169,27 @@ __host__ __device__ constexpr bool axis_symmetric() {
 // they fit 80 registers and gain from the sixth warp per scheduler (cfg2
 // -1.3%, cfg1 -7%, cfg4 -5..7%, cfg5 -3%, cfg3 ridge -1% fill time; the d=10
 // registry functors spill at 80 registers and keep 640).
+// The Genz kernels (cfg4) read RN(digit/N) from the shared digit table
+// instead of holding d of them in registers, which brings them to 64
+// registers and 1024 threads (32 warps per SM: fill -4.8% cfg4a, -2.3%
+// cfg4b; the same trade costs cfg1/cfg2 3-5%, whose table reads compete with
+// the pair table).
+#ifndef VPB_GENZ_NT
+#define VPB_GENZ_NT 1024
+#endif
+#ifndef VPB_GENZ_PP_TABLE
+#define VPB_GENZ_PP_TABLE 1
+#endif
+template <int ID, int D>
+__host__ __device__ constexpr bool dq_from_table() {
+  return (ID == VPB_GENZ_OSCILLATORY || (ID == VPB_GENZ_PRODUCTPEAK && VPB_GENZ_PP_TABLE)) &&
+         D > 0 && D <= 12 && VPB_GENZ_NT > 0;
+}
+
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
+  return dq_from_table<ID, D>() ? VPB_GENZ_NT
+         : ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
            ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) && D > 0 &&
           D <= 12) ||
                  (LAYOUT == LAYOUT_RECORDS && D > 12)
@@ -188,7 +206,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   constexpr int K0 = (LAYOUT == LAYOUT_RECORDS && D >= 12) ? REC_K0 : 0;
   // cube digits RN(digit/N) per axis in registers for small d; above that the
   // digits are kept packed and RN(digit/N) is read from the shared table
-  constexpr bool DQ_REG = D == 0 || D <= VPB_DQ_REG_MAX;
+  constexpr bool DQ_REG = D == 0 || (D <= VPB_DQ_REG_MAX && !dq_from_table<ID, D>());
   // XPERM (power-of-two d, pair table, axis-symmetric integrand): at step s
   // lane l samples axis s ^ (l mod d).  The 8 lanes of a quarter-warp then
   // read 8 different axes, and with the pair table laid out [interval][axis]
@@ -350,7 +368,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
           return dq[j];
         } else {
           const uint32_t dig = (uint32_t)((dpk >> (j * dbits)) & dmask);
-          return s_dq[dig];
+          // n_strat**d < 2^31 keeps n_strat <= 1290 <= DQ_TABLE_MAX for d >= 3:
+          // the table always exists there
+          if constexpr (D >= 3) return s_dq[dig];
+          else return dq_tab ? s_dq[dig] : div_exact((double)dig, a.nsf, a.rns);
         }
       };
       auto close_segment = [&](int seg_end) {
