@@ -167,28 +167,33 @@ __host__ __device__ constexpr bool axis_symmetric() {
 // the kernels whose integrand sums are streamed (Gaussian, 3-peak Gaussian:
 // StreamSum keeps few partials live) and the many-axis records kernels --
 // they fit 80 registers and gain from the sixth warp per scheduler (cfg2
-// -1.3%, cfg1 -7%, cfg4 -5..7%, cfg5 -3%, cfg3 ridge -1% fill time; the d=10
-// registry functors spill at 80 registers and keep 640).
-// The Genz kernels (cfg4) read RN(digit/N) from the shared digit table
-// instead of holding d of them in registers, which brings them to 64
-// registers and 1024 threads (32 warps per SM: fill -4.8% cfg4a, -2.3%
-// cfg4b; the same trade costs cfg1/cfg2 3-5%, whose table reads compete with
-// the pair table).
-#ifndef VPB_GENZ_NT
-#define VPB_GENZ_NT 1024
+// -1.3%, cfg1 -7%, cfg4 -5..7%, cfg5 -3%, cfg3 ridge -1% fill time), or
+// 1024 in table mode (below); the rest keep 640.
+// Table mode: RN(digit/N) read from the shared digit table instead of d
+// registers, which brings these kernels to 64 registers and 1024 threads
+// (32 warps per SM).  Measured fill time: Genz oscillatory -4.8% (cfg4a),
+// product peak -2.3% (cfg4b), Roos & Arnold -8.5%, linear -7.8%, Morokoff
+// -3.9%, exponential -3.3%, path integral -3.0%; cosine (+0.9%, its cos
+// spills) and the streamed Gaussians (cfg1/cfg2 +3-5%: their table reads
+// compete with the pair table) keep the digits in registers.
+#ifndef VPB_TABLE_NT
+#define VPB_TABLE_NT 1024
 #endif
-#ifndef VPB_GENZ_PP_TABLE
-#define VPB_GENZ_PP_TABLE 1
+#ifndef VPB_REC_NT
+#define VPB_REC_NT VPB_STREAM_NT
 #endif
 template <int ID, int D>
 __host__ __device__ constexpr bool dq_from_table() {
-  return (ID == VPB_GENZ_OSCILLATORY || (ID == VPB_GENZ_PRODUCTPEAK && VPB_GENZ_PP_TABLE)) &&
-         D > 0 && D <= 12 && VPB_GENZ_NT > 0;
+  return (ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_ROOS_ARNOLD ||
+          ID == VPB_LINEAR || ID == VPB_EXPONENTIAL || ID == VPB_MOROKOFF ||
+          ID == VPB_PATH_INTEGRAL) &&
+         D >= 3 && D <= 12 && VPB_TABLE_NT > 0;
 }
 
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return dq_from_table<ID, D>() ? VPB_GENZ_NT
+  return dq_from_table<ID, D>() ? VPB_TABLE_NT
+         : (LAYOUT == LAYOUT_RECORDS && D > 12) ? VPB_REC_NT
          : ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
            ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) && D > 0 &&
           D <= 12) ||
