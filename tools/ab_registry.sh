@@ -1,3 +1,4 @@
+# A/B table mode on the registry functors: default build vs _lib/variants/reg (built with the candidate defines); prints fill ms per iteration
 for spec in "linear 10" "cosine 10" "exponential 10" "morokoff 8" "path_integral 7" "roos_arnold 10"; do
   set -- $spec
   for lib in default reg; do
