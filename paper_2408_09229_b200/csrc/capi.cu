@@ -498,17 +498,18 @@ int enqueue_update(vpb_ctx *c, int record) {
   return VPB_OK;
 }
 
-__global__ void mark_fail_kernel(const int *status, int *fail_it, const Sched *sched) {
-  if (*status && *fail_it < 0) *fail_it = sched->it;
-}
-// iteration index lives on device (so one captured graph serves every
-// iteration); frozen once an iteration failed
-__global__ void step_it_kernel(Sched *sched, const int *status) {
-  if (!*status) sched->it = sched->it + 1;
+// End of an iteration: record the first failing iteration, else advance the
+// device-side iteration index (so one captured graph serves every
+// iteration; the index freezes once an iteration failed).
+__global__ void end_iteration_kernel(const int *status, int *fail_it, Sched *sched) {
+  if (*status) {
+    if (*fail_it < 0) *fail_it = sched->it;
+  } else {
+    sched->it = sched->it + 1;
+  }
 }
 
 int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
-  step_it_kernel<<<1, 1, 0, c->st>>>(c->sched, c->status);
   CK(rec_event(c, E[0]));
   TRY(enqueue_plan(c, 1, nullptr));
   CK(rec_event(c, E[1]));
@@ -516,7 +517,7 @@ int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
   CK(rec_event(c, E[4]));
   TRY(enqueue_update(c, 1));
   CK(rec_event(c, E[5]));
-  mark_fail_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
+  end_iteration_kernel<<<1, 1, 0, c->st>>>(c->status, c->fail_it, c->sched);
   CK(cudaGetLastError());
   return VPB_OK;
 }
@@ -910,7 +911,7 @@ int vpb_reset(vpb_ctx *c) {
   CK(cudaStreamSynchronize(c->st));
   TRY(upload_uniform_edges(c));
   Sched s{};
-  s.it = -1;   // step_it_kernel pre-increments
+  s.it = 0;   // end_iteration_kernel advances it
   CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
   Scalars z{};
   CK(cudaMemcpy(c->sc, &z, sizeof(z), cudaMemcpyHostToDevice));
@@ -1047,10 +1048,10 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   if (layout) *layout = c->layout;
   if (n_chunks) *n_chunks = c->records ? c->n_chunks : 0;
   // plan_scan, plan_offsets, fill | chunks x (fill + groups), fixup, histogram
-  // reduce, cube_terms, results_leaf, results_tree, alloc, refine, step, mark
+  // reduce, cube_terms, results_leaf, results_tree, alloc, refine, end
   const int n_rec = c->dims - c->rec_k0;
   const int fill = c->records ? c->n_chunks * (1 + (n_rec >= 8) + (n_rec % 8 != 0)) : 1;
-  if (launches) *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 2;
+  if (launches) *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1;
   return VPB_OK;
 }
 
