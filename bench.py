@@ -286,6 +286,26 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
                 traffic = json.load(open(tp)).get(cfgname)
             except Exception:
                 traffic = None
+        # SURVEY 8(d)'s issue-bound variant: the fill's executed instructions
+        # per evaluation (ncu smsp__inst_executed.sum of one fill launch,
+        # profiles/fill_traffic.json "inst_per_eval") at the measured rate,
+        # against 4 warp-instructions per clock per SM at the sampled clock
+        issue = None
+        try:
+            ipe = json.load(open(tp)).get("inst_per_eval", {}).get(cfgname)
+        except Exception:
+            ipe = None
+        clk = clocks.summary()
+        mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz")
+        if ipe and mhz:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            warp_ips = evals_per_rank / (fill_ms_max * 1e-3) * ipe / 32.0
+            ipeak = sms * 4 * mhz * 1e6
+            issue = {"inst_per_eval": ipe, "achieved": warp_ips / 1e12, "peak": ipeak / 1e12,
+                     "unit": "T warp-instr/s", "frac": warp_ips / ipeak,
+                     "source": "lane instructions per evaluation from ncu (profiles/"
+                               "fill_traffic.json); peak = 4 issue slots/clk/SM x SMs x "
+                               "sampled SM clock"}
         cpu = None
         if world == 1 and not args.no_cpu:
             sample = int(os.environ.get("VPB_CPU_SAMPLE", cfg["n_eval"] // 10))
@@ -315,12 +335,12 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
                                        "counts); peak = measured DFMA rate on this GPU "
                                        "(vpb_fp64_peak)",
                          "ops_per_eval": ops, "fill_kernel_ms_per_step": fill_ms_max / steps,
-                         "fill_share_of_step": fill_ms_max / t_max},
+                         "fill_share_of_step": fill_ms_max / t_max, "issue": issue},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": layout["launches_per_iteration"] * steps,
-            "clocks": clocks.summary(),
+            "clocks": clk,
             "estimates": {"last": float(est[-1]), "sigma_last": float(np.sqrt(var[-1]))},
         }
         print(json.dumps(line), flush=True)

@@ -15,8 +15,8 @@ bash tools/gpu_profile.sh cfg2 $TAG/p
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 2 -c 1 \
   -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 4 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
 # DRAM bytes of one fill launch per config (roofline.traffic; base units)
-for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5; do
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5 ra10; do
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum \
     --print-units base --clock-control none --csv -k regex:fill_kernel -s 2 -c 1 \
     --log-file gpurun_out/$TAG/traffic_$c.csv python tools/profile_fill.py $c 3 > /dev/null 2>&1
   echo "traffic $c rc=$?"

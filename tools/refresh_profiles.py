@@ -78,11 +78,17 @@ for f in sorted(os.listdir(src)):
     if os.path.exists(bl):
         chunks = max(1, int(json.load(open(bl))["config"].get("record_chunks") or 1))
     t[cfg] = int(per_launch * chunks)
+    ins = by.get("smsp__inst_executed.sum")
+    if ins and os.path.exists(bl):
+        evals = float(json.load(open(bl))["config"]["evals_per_step"])
+        t.setdefault("inst_per_eval", {})[cfg] = round(ins * chunks * 32.0 / evals, 1)
     found = True
 if found:
     t["_note"] = ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, ncu) of the fill "
                   "kernel per step: one launch x the record chunks per iteration (cfg5), "
-                  "captured by tools/gpu_checkpoint.sh into profiles/%s/traffic_*.csv" % rnd)
+                  "captured by tools/gpu_checkpoint.sh into profiles/%s/traffic_*.csv; "
+                  "inst_per_eval = smsp__inst_executed.sum x 32 / evaluations (lane "
+                  "instructions per evaluation, the issue-bound roofline)" % rnd)
     for f in os.listdir(src):
         if f.startswith("traffic_") and f.endswith(".csv"):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
