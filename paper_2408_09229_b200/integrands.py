@@ -62,7 +62,7 @@ PATH_BOX_HALF_WIDTH = 5.0
 class UnknownIntegrandError(VegasError, LookupError):
     def __init__(self, name):
         super().__init__(
-            f"unknown integrand {name!r}; available: {', '.join(available())}")
+            f"unknown integrand {name!r}; available: {', '.join(available_all())}")
 
 
 class DeviceIntegrand:
@@ -349,8 +349,21 @@ BENCHMARK_NAMES = ("sinexp", "linear", "cosine", "exponential",
                    "roos_arnold", "morokoff", "gaussian", "ridge")
 
 
+#: the reference's registry (vp/integrands.py:399-415); the BASELINE-pinned
+#: functions and `constant` are extras, reachable by name through lookup()
+REFERENCE_NAMES = ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff",
+                   "gaussian", "ridge", "asian_option", "path_integral")
+
+
 def available() -> list[str]:
-    return sorted(_BUILDERS) + ["constant"]
+    """The registry's names, as the reference reports them (vp/integrands.py:417-418)."""
+    return sorted(REFERENCE_NAMES)
+
+
+def available_all() -> list[str]:
+    """Every name lookup() accepts: the reference's registry plus the
+    BASELINE-pinned integrands (multipeak8, genz_*6, gaussian20) and constant."""
+    return sorted(set(_BUILDERS) | {"constant"})
 
 
 def constant(value: float, dims: int = 1) -> IntegrandSpec:
