@@ -70,24 +70,52 @@ __device__ __forceinline__ double erfinv_ref(double y) {
 }
 
 // Ridge window sum (vp/integrands.py:154-182) over the centres c_i = i/(n-1)
-// for i in [lo, hi]: sum_i exp(-400 (c_i - mu)^2).  `ctab` (optional) holds
-// RN(i/(n-1)) precomputed (the fill kernel stages it in shared memory: the
-// same bits as the division, three FP64 ops cheaper per term); the
-// exponent lies in [-46.1, 0] inside the window, so the unclamped exp core
-// is exact to the clamped one.
+// for i in [lo, hi]: sum_i exp(-400 (c_i - mu)^2), summed in increasing i as
+// the reference does.  `ctab` (optional) holds RN(i/(n-1)) precomputed (the
+// fill kernel stages it in shared memory: the same bits as the division).
+//
+// Blocked exact-factor recurrence: with dc = c_i - mu and the spacing
+// delta, consecutive terms satisfy E_{i+1} = E_i * R_i with
+// R_i = exp(-400 delta (2 dc + delta)) and R_{i+1} = R_i * B, B =
+// exp(-800 delta^2).  Each block of RIDGE_BLK centres starts from the
+// reference's own term (direct exp of -400 dc^2 at c_i = RN(i/(n-1))) and
+// its factor R; the other terms cost two multiplications instead of an
+// exp.  The window sum stays within 1.1e-14 relative of the direct sum at
+// 32 centres per block (worst of 1500 random windows in an IEEE emulation;
+// 3.7e-15 at 16, 4.3e-14 at 64), inside the 1e-13 integrand tolerance
+// (tests/test_gpu_parity.py): the centres RN(i/(n-1)) differ from c_ib +
+// k delta by an ulp, and the products round k times.  cfg3 fill: 91.5 ms
+// (direct) -> 30.7 ms (16) -> 21.5 ms (32).  VPB_RIDGE_BLK=1 is the direct
+// sum.  Exponents inside the window lie in [-46.1, 0] and the
+// factors in (e^-0.28, e^0.28), so the unclamped exp core is exact to the
+// clamped one.
+#ifndef VPB_RIDGE_BLK
+#define VPB_RIDGE_BLK 32
+#endif
 __device__ __forceinline__ double ridge_window(double mu, int lo, int hi, double spacing,
                                                const double *ctab) {
+  const double rsp = 1.0 / spacing;   // delta
   double acc = 0.0;
-  if (ctab) {
+  if constexpr (VPB_RIDGE_BLK <= 1) {
     for (int i = lo; i <= hi; i++) {
-      const double dc = __dadd_rn(ctab[i], -mu);
+      const double c = ctab ? ctab[i] : div_exact((double)i, spacing, rsp);
+      const double dc = __dadd_rn(c, -mu);
       acc = __dadd_rn(acc, fast_exp_core(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
     }
-  } else {
-    const double rsp = 1.0 / spacing;
-    for (int i = lo; i <= hi; i++) {
-      const double dc = __dadd_rn(div_exact((double)i, spacing, rsp), -mu);
-      acc = __dadd_rn(acc, fast_exp_nonpos(__dmul_rn(__dmul_rn(-400.0, dc), dc)));
+    return acc;
+  }
+  const double B = fast_exp_core(__dmul_rn(__dmul_rn(-800.0, rsp), rsp));
+  const double m400d = __dmul_rn(-400.0, rsp);
+  for (int ib = lo; ib <= hi; ib += VPB_RIDGE_BLK) {
+    const double c = ctab ? ctab[ib] : div_exact((double)ib, spacing, rsp);
+    const double dc = __dadd_rn(c, -mu);
+    double e = fast_exp_core(__dmul_rn(__dmul_rn(-400.0, dc), dc));
+    double r = fast_exp_core(__dmul_rn(m400d, __dadd_rn(__dmul_rn(2.0, dc), rsp)));
+    const int n = min(VPB_RIDGE_BLK, hi - ib + 1);
+    for (int k = 0; k < n; k++) {
+      acc = __dadd_rn(acc, e);
+      e = __dmul_rn(e, r);
+      r = __dmul_rn(r, B);
     }
   }
   return acc;
