@@ -269,6 +269,7 @@ struct vpb_ctx {
   long long rec_ch = 0;        // runs per chunk (multiple of FILL_TILE)
   int rec_k0 = 0;              // leading axes the records-layout fill keeps in shared memory
   int n_chunks = 0, n_groups = 0, rec_B = 0;
+  long long rec_cap_runs = 0;   // runs the record chunks cover for world = 1
   unsigned short *rec_iv = nullptr;
   double *rec_w2 = nullptr, *hw_rec = nullptr;
   unsigned *hc_rec = nullptr;
@@ -818,6 +819,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     if (ch < FILL_TILE) ch = FILL_TILE;
     c->rec_ch = std::min(ch, cap_runs);
     c->n_chunks = (int)((cap_runs + c->rec_ch - 1) / c->rec_ch);
+    c->rec_cap_runs = cap_runs;
     const size_t hsm = hist_records_smem(c->ng);
     int hr_per_sm = 0;
 #define VPB_HR_ATTR(J)                                                                        \
@@ -881,6 +883,21 @@ int vpb_nccl_unique_id(char id_out[128]) {
   return VPB_OK;
 }
 
+// Record chunks for this rank's shard: a shard holds at most
+// ceil(cap / world) runs, so the chunk loop need not walk the whole plan's
+// tile range (tiles are shard-relative).
+static void shard_chunks(vpb_ctx *c) {
+  if (!c->records || c->rec_cap_runs <= 0) return;
+  if (c->world <= 1) {
+    c->n_chunks = (int)((c->rec_cap_runs + c->rec_ch - 1) / c->rec_ch);
+    return;
+  }
+  const long long shard = (c->rec_cap_runs + c->world - 1) / c->world;
+  const long long tiles = (shard + FILL_TILE - 1) / FILL_TILE + 1;
+  const long long tpc = c->rec_ch / FILL_TILE;
+  c->n_chunks = (int)std::max(1ll, (tiles + tpc - 1) / tpc);
+}
+
 int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank) {
   if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
   TRY(setdev(c));
@@ -894,6 +911,7 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
   NK(ncclCommInitRank(&c->comm, world, uid, rank));
   c->world = world;
   c->rank = rank;
+  shard_chunks(c);
   return VPB_OK;
 }
 
@@ -901,6 +919,7 @@ int vpb_set_shard(vpb_ctx *c, int32_t world, int32_t rank) {
   if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
   c->world = world;
   c->rank = rank;
+  shard_chunks(c);
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
   if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   return VPB_OK;

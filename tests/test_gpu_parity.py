@@ -305,6 +305,33 @@ def test_iteration_shards_merge_to_whole(world):
     np.testing.assert_allclose(sum(p[3] for p in parts), whole[3], rtol=1e-12, atol=1e-290)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_record_chunk_shards_merge_to_whole(monkeypatch, world):
+    # records layout forced with small chunks: each rank's chunk loop covers
+    # only its shard's tiles (vpb_set_shard sizes it), and the shards still
+    # sum to the whole fill
+    monkeypatch.setenv("VPB_FILL_LAYOUT", "records")
+    monkeypatch.setenv("VPB_REC_CHUNK", "8192")
+    cfg = P.IntegratorConfig(n_eval=200_000, max_it=3, n_intervals=64, seed=5, batch_size=4096)
+
+    def run(w, r):
+        with P.Integrator("gaussian20", [(0.0, 1.0)] * 20, cfg) as it:
+            if w > 1:
+                it.set_shard(w, r)
+            lay = it.fill_layout()
+            it.fill(777)
+            return it.accumulators(), lay
+
+    whole, lw = run(1, 0)
+    parts = [run(world, r) for r in range(world)]
+    assert lw["chunks"] > 1 and all(p[1]["chunks"] < lw["chunks"] for p in parts)
+    acc = [p[0] for p in parts]
+    np.testing.assert_array_equal(sum(p[1] for p in acc), whole[1])
+    np.testing.assert_array_equal(sum(p[4] for p in acc), whole[4])
+    np.testing.assert_allclose(sum(p[0] for p in acc), whole[0], rtol=1e-12)
+    np.testing.assert_allclose(sum(p[2] for p in acc), whole[2], rtol=1e-12, atol=1e-290)
+
+
 @pytest.mark.parametrize("traj,name", [("traj_gauss4_small.npz", "gaussian"),
                                        ("traj_ridge_small.npz", "ridge"),
                                        ("traj_genzosc_small.npz", "genz_oscillatory6"),
