@@ -250,6 +250,23 @@ def test_sharded_fill_merge_gloo_world2():
     assert q.get(timeout=10) is True
 
 
+def test_reference_arm_under_torchrun_world2():
+    """The driver's N>1 launch of the reference arm: rank 0 alone prints the
+    one JSON line, the other rank exits 0 without work."""
+    env = dict(os.environ, VPB_REF_SAMPLE="100000")
+    port = str(29600 + os.getpid() % 300)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", port, os.path.join(ROOT, "bench.py"), "--impl",
+                          "reference", "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+
+
 def test_reference_arm_json_line():
     env = dict(os.environ, VPB_REF_SAMPLE="200000")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
