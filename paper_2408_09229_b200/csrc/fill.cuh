@@ -195,14 +195,12 @@ __host__ __device__ constexpr bool dq_from_table() {
 
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return dq_from_table<ID, D>() ? VPB_TABLE_NT
-         : (LAYOUT == LAYOUT_RECORDS && D > 12) ? VPB_REC_NT
+  return dq_from_table<ID, D>()                      ? VPB_TABLE_NT
+         : (LAYOUT == LAYOUT_RECORDS && D > 12)      ? VPB_REC_NT
          : ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
-           ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) && D > 0 &&
-          D <= 12) ||
-                 (LAYOUT == LAYOUT_RECORDS && D > 12)
-             ? VPB_STREAM_NT
-             : FILL_NT;
+             ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) &&
+            D > 0 && D <= 12)                        ? VPB_STREAM_NT
+                                                     : FILL_NT;
 }
 
 template <int ID, int D, int LAYOUT>
