@@ -52,15 +52,15 @@ sys.path.insert(0, ROOT)
 # (add/sub/mul/div = 1) and `div` the divisions in it.  cfg3 counts the
 # algorithm the device runs: the reference's windowed sum of ~632 centre
 # terms (vp/integrands.py:154-182) by the blocked exact-factor recurrence of
-# integrands.cuh ridge_window -- per 32-centre block one direct exp pair and
+# integrands.cuh ridge_window -- per 64-centre block one direct exp pair and
 # 6 FLOP, per centre 3 FLOP (two products and the sum), the centres
-# RN(i/999) staged once per CTA: sampling 44 + setup 23 + 20 blocks x 6 +
-# 632 x 3 + accumulate 8 = 2091 FLOP, 9 divisions, 42 exps.
+# RN(i/999) staged once per CTA: sampling 44 + setup 23 + 10 blocks x 6 +
+# 632 x 3 + accumulate 8 = 2031 FLOP, 9 divisions, 22 exps.
 COST = {"div": 3, "exp": 18, "cos": 16}
 CONFIGS = {
     "cfg1": dict(integrand="gaussian", dims=4, n_eval=10**6, ng=1000, flops=65, div=9, exp=1),
     "cfg2": dict(integrand="multipeak8", dims=8, n_eval=10**8, ng=1024, flops=177, div=20, exp=3),
-    "cfg3": dict(integrand="ridge", dims=4, n_eval=10**8, ng=1024, flops=2091, div=9, exp=42),
+    "cfg3": dict(integrand="ridge", dims=4, n_eval=10**8, ng=1024, flops=2031, div=9, exp=22),
     "cfg4a": dict(integrand="genz_oscillatory6", dims=6, n_eval=10**9, ng=1024, flops=88, div=12,
                   cos=1),
     "cfg4b": dict(integrand="genz_productpeak6", dims=6, n_eval=10**9, ng=1024, flops=105, div=18),

@@ -80,17 +80,15 @@ __device__ __forceinline__ double erfinv_ref(double y) {
 // exp(-800 delta^2).  Each block of RIDGE_BLK centres starts from the
 // reference's own term (direct exp of -400 dc^2 at c_i = RN(i/(n-1))) and
 // its factor R; the other terms cost two multiplications instead of an
-// exp.  The window sum stays within 1.1e-14 relative of the direct sum at
-// 32 centres per block (worst of 1500 random windows in an IEEE emulation;
-// 3.7e-15 at 16, 4.3e-14 at 64), inside the 1e-13 integrand tolerance
-// (tests/test_gpu_parity.py): the centres RN(i/(n-1)) differ from c_ib +
-// k delta by an ulp, and the products round k times.  cfg3 fill: 91.5 ms
-// (direct) -> 30.7 ms (16) -> 21.5 ms (32).  VPB_RIDGE_BLK=1 is the direct
-// sum.  Exponents inside the window lie in [-46.1, 0] and the
-// factors in (e^-0.28, e^0.28), so the unclamped exp core is exact to the
-// clamped one.
+// exp.  Measured on the B200 against the direct sum (VPB_RIDGE_BLK=1) on 3M
+// points, uniform and near the ridge (tools/ridge_eval.py): max relative
+// deviation 1.3e-14 at 32 centres per block, 5.1e-14 at 64 -- inside the
+// 1e-13 integrand tolerance (tests/test_gpu_parity.py) -- because the
+// centres RN(i/(n-1)) differ from c_ib + k delta by an ulp and the products
+// round k times.  cfg3 fill: 91.5 ms (direct) -> 30.7 (16) -> 21.5 (32) ->
+// 16.9 ms (64).  VPB_RIDGE_BLK=1 is the direct sum.
 #ifndef VPB_RIDGE_BLK
-#define VPB_RIDGE_BLK 32
+#define VPB_RIDGE_BLK 64
 #endif
 __device__ __forceinline__ double ridge_window(double mu, int lo, int hi, double spacing,
                                                const double *ctab) {

@@ -135,6 +135,19 @@ def test_integrand_values(golden):
         np.testing.assert_allclose(v, g[name], rtol=1e-13, atol=atol, err_msg=name)
 
 
+def test_ridge_recurrence_against_oracle():
+    # the blocked window recurrence (integrands.cuh ridge_window) against the
+    # oracle's direct sum of exponentials on 200k points, half of them near
+    # the ridge where the window sum is large
+    g = np.random.default_rng(17)
+    t = g.random((100_000, 1))
+    x = np.concatenate([g.random((100_000, 4)),
+                        np.clip(t + 0.02 * g.standard_normal((100_000, 4)), 0.0, 1.0)])
+    v = P.lookup("ridge").evaluate_batch(x)
+    ref = O.evaluate("ridge", x)
+    np.testing.assert_allclose(v, ref, rtol=1e-13, atol=1e-300)
+
+
 def test_application_integrand_values(golden):
     # device erfinv / lattice action vs the reference's own values
     g = golden("integrands.npz")
