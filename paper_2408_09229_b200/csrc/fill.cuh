@@ -413,9 +413,9 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
           if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {   // s += x_j a_j
             gz = __dadd_rn(gz, __dmul_rn(xs, a.P.p[1 + step]));
-          } else if constexpr (GSTREAM) {   // prod *= 1 / (a_j^-2 + (x_j - u_j)^2)
+          } else if constexpr (GSTREAM) {   // den *= a_j^-2 + (x_j - u_j)^2
             const double u = __dadd_rn(xs, -a.P.p[D + step]);
-            gz = __dmul_rn(gz, __drcp_rn(__dadd_rn(a.P.p[step], __dmul_rn(u, u))));
+            gz = __dmul_rn(gz, __dadd_rn(a.P.p[step], __dmul_rn(u, u)));
           }
           if constexpr (STREAM) {
 #pragma unroll
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         } else if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {
           f = cos(__dadd_rn(a.P.p[0], gz));   // cos(2 pi u_1 + a.x)
         } else if constexpr (GSTREAM) {
-          f = gz;
+          f = __drcp_rn(gz);   // 1 / prod of the denominators (integrands.cuh)
         } else {
           f = integrand<ID, D>(x, d, a.P, RTAB ? s_ctab : nullptr);
         }

@@ -214,15 +214,17 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     }
     return cos(__dadd_rn(P.p[0], s));
   } else if constexpr (ID == VPB_GENZ_PRODUCTPEAK) {
-    // prod_j 1 / (a_j^-2 + (x_j - u_j)^2)
-    double prod = 1.0;
+    // prod_j 1 / (a_j^-2 + (x_j - u_j)^2), as 1 / prod_j (...): one exact
+    // reciprocal instead of d (a few ulp from the per-factor form; the
+    // denominators lie in [a_j^-2, a_j^-2 + 1], no overflow)
+    double den = 1.0;
     const int dd = D > 0 ? D : d;
 #pragma unroll
     for (int j = 0; j < (D > 0 ? D : d); j++) {
       const double u = __dadd_rn(x[j], -P.p[dd + j]);
-      prod = __dmul_rn(prod, __drcp_rn(__dadd_rn(P.p[j], __dmul_rn(u, u))));
+      den = __dmul_rn(den, __dadd_rn(P.p[j], __dmul_rn(u, u)));
     }
-    return prod;
+    return __drcp_rn(den);
   } else if constexpr (ID == VPB_SINEXP) {
     return __dadd_rn(sin(x[0]), fast_exp(x[1]));   // vp/integrands.py:106-107
   } else if constexpr (ID == VPB_LINEAR) {
