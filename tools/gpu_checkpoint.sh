@@ -4,6 +4,16 @@
 # capture of the fill kernel.   tools/gpu_checkpoint.sh TAG
 TAG=${1:-ck}
 mkdir -p gpurun_out/$TAG
+# DRAM bytes of one fill launch per config (roofline.traffic; base units)
+for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5 ra10; do
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum \
+    --print-units base --clock-control none --csv -k regex:fill_kernel -s 2 -c 1 \
+    --log-file gpurun_out/$TAG/traffic_$c.csv python tools/profile_fill.py $c 3 > /dev/null 2>&1
+  echo "traffic $c rc=$?"
+done
+# instruction counts into profiles/fill_traffic.json before the bench lines
+# read them (roofline.issue)
+python tools/refresh_profiles.py gpurun_out/$TAG round1 > /dev/null
 timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/$TAG/tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/$TAG/tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/$TAG/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 600 python bench.py > gpurun_out/$TAG/bench_default.json 2> gpurun_out/$TAG/bench_default.err; echo "bench rc=$?"; cat gpurun_out/$TAG/bench_default.json
@@ -14,10 +24,3 @@ done
 bash tools/gpu_profile.sh cfg2 $TAG/p
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 2 -c 1 \
   -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 4 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
-# DRAM bytes of one fill launch per config (roofline.traffic; base units)
-for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5 ra10; do
-  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum \
-    --print-units base --clock-control none --csv -k regex:fill_kernel -s 2 -c 1 \
-    --log-file gpurun_out/$TAG/traffic_$c.csv python tools/profile_fill.py $c 3 > /dev/null 2>&1
-  echo "traffic $c rc=$?"
-done
