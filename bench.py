@@ -8,10 +8,14 @@ Contract (BASELINE.json metric; one JSON line from rank 0):
 
 * workload: BASELINE.json configs[1] = cfg2, the 8-D three-peak Gaussian
   (multipeak8), n_eval = 1e8 per iteration per GPU (weak scaling: N GPUs
-  integrate n_eval = N * 1e8 with the same cube geometry, runs sharded by the
-  reference's partition rule and merged by one NCCL all-reduce), FP64,
-  n_intervals 1024, alpha 0.5, beta 0.75.  Synthetic: the integrand is a
-  closed-form function, nothing is loaded.
+  integrate n_eval = N * 1e8 with the same cube geometry), FP64, n_intervals
+  1024, alpha 0.5, beta 0.75.  BASELINE's multi-GPU configurations (cfg4a/b:
+  1e9, cfg5: 4e9 per iteration in total) default to strong scaling
+  (--scaling strong: the fixed total split over the N GPUs).  Runs are sharded
+  by hypercube range (the reference's partition rule, each split point
+  snapped to the next cube start) and merged by one NCCL all-reduce per
+  iteration.  Synthetic: the integrand is a closed-form function, nothing is
+  loaded.
 * a step = one full iteration (plan -> fused fill -> [all-reduce] ->
   results -> allocation -> refine) on device.  W warm-up iterations, then K
   timed iterations; L2 is flushed (256 MiB write) before every timed
@@ -150,6 +154,39 @@ def cpu_oracle_rate(cfg, n_eval_sample: int, iters: int = 2, workers: int | None
     return out.evals[-1] / out.fill_seconds[-1], workers, out
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (BASELINE.md §2 asks for it with the core count)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline(cfg) -> dict:
+    """The oracle on all host threads (the reported value) and on one thread
+    (W = all cores and W = 1), same cube geometry at a bounded
+    n_eval sample; fill time of iteration 2 only."""
+    sample = int(os.environ.get("VPB_CPU_SAMPLE", cfg["n_eval"] // 10))
+    # one thread gets a tenth of the sample (same geometry: the cube cap
+    # binds), keeping the leg within seconds
+    sample1 = max(10 ** 6, sample // 10)
+    rate, cores, _ = cpu_oracle_rate(cfg, sample)
+    rate1, _, _ = cpu_oracle_rate(cfg, sample1, workers=1)
+    return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+            "sample": f"oracle (C port of vp/executor.parallel_fill, {cores} threads) "
+                      f"iteration 2 of {cfg['integrand']} at n_eval={sample} (same cube "
+                      f"geometry as n_eval={cfg['n_eval']}); fill time only",
+            "single_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                              "sample": f"iteration 2 at n_eval={sample1}, 1 thread"},
+            "thread_speedup": rate / rate1 if rate1 > 0 else None}
+
+
 # ------------------------------------------------------------------ arms --
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -196,10 +233,11 @@ def run_reference(args, cfgname, cfg, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfgname}: {cfg['integrand']} d={cfg['dims']} "
                                f"ng={cfg['ng']}", "n_eval_per_iteration": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.warmup + args.steps} oracle iterations of "
                                    f"{cfg['integrand']} at n_eval={sample} (same cube geometry "
                                    f"as n_eval={cfg['n_eval']}); fill time only"},
@@ -218,7 +256,9 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    n_eval = cfg["n_eval"] * world          # weak scaling: fixed work per GPU
+    # weak: fixed work per GPU (n_eval x N); strong: BASELINE's fixed total
+    # (cfg4's 1e9 and cfg5's 4e9 per iteration split over the N GPUs)
+    n_eval = cfg["n_eval"] * world if args.scaling == "weak" else cfg["n_eval"]
     steps, warmup = args.steps, args.warmup
     conf = P.IntegratorConfig(n_eval=n_eval, max_it=warmup + steps + 1,
                               n_intervals=cfg["ng"])
@@ -313,22 +353,20 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
                                "sampled SM clock"}
         cpu = None
         if world == 1 and not args.no_cpu:
-            sample = int(os.environ.get("VPB_CPU_SAMPLE", cfg["n_eval"] // 10))
-            rate, cores, _ = cpu_oracle_rate(cfg, sample)
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"oracle (C port of vp/executor.parallel_fill, {cores} threads) "
-                             f"iteration 2 of {cfg['integrand']} at n_eval={sample} (same cube "
-                             f"geometry as n_eval={cfg['n_eval']}); fill time only"}
+            cpu = cpu_baseline(cfg)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warmup, "ms_per_step": t_max / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (closed-form integrand, nothing loaded)",
             "config": {"workload": f"{cfgname}: {cfg['integrand']} d={cfg['dims']}, "
-                                   f"n_eval={cfg['n_eval']:.0e}/iter/GPU, ng={cfg['ng']}",
+                                   f"n_eval={cfg['n_eval']:.0e}/iter"
+                                   f"{'/GPU' if args.scaling == 'weak' else ' in total'}, "
+                                   f"ng={cfg['ng']}",
                        "n_eval_per_iteration": n_eval, "n_strat": integ.n_strat,
                        "n_cubes": integ.n_cubes, "evals_per_step": evals_timed / steps,
-                       "parallelism": f"runs sharded over {world} GPU(s), NCCL all-reduce",
+                       "parallelism": f"hypercube-aligned run shards over {world} GPU(s), "
+                                      f"one NCCL all-reduce per iteration",
                        "l2": "flushed (256 MiB write) before every timed iteration",
                        "fill_layout": layout["layout"], "record_chunks": layout["chunks"]},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12,
@@ -360,7 +398,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: n_eval per GPU; strong: n_eval in total (default: strong for "
+                         "BASELINE's multi-GPU configs cfg4a/cfg4b/cfg5, weak otherwise)")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.config in ("cfg4a", "cfg4b", "cfg5") else "weak"
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]

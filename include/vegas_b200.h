@@ -99,6 +99,10 @@ const char *vpb_last_error(void);
 /* 1 if the integrand id is compiled for this dimension with the fast
  * (compile-time dims) fill kernel, 0 if it runs the generic kernel. */
 int vpb_is_specialised(int32_t integrand, int32_t dims);
+/* Number of CUDA devices visible to this process (CUDA_VISIBLE_DEVICES
+ * applies); 0 and VPB_OK when there is none.  The host maps LOCAL_RANK onto
+ * an ordinal with it (LOCAL_RANK mod count). */
+int vpb_device_count(int32_t *n);
 
 /* ---- context: the state of one integrate() call (vp/core.py:168-238) ------ */
 int vpb_create(const vpb_desc *desc, vpb_ctx **out);
@@ -112,6 +116,19 @@ int vpb_nccl_unique_id(char id_out[128]);
 int vpb_attach_nccl(vpb_ctx *ctx, const char id[128], int32_t world, int32_t rank);
 /* Shard without NCCL (the host merges accumulators itself). */
 int vpb_set_shard(vpb_ctx *ctx, int32_t world, int32_t rank);
+/* Multi-rank without NCCL: the per-iteration exchange (the same three
+ * reductions the NCCL path makes: map_w|s1|s2 f64 SUM, map_counts i64 SUM,
+ * the 3-word control word i64 MAX -- failure flags and the first failing
+ * run, so every rank raises the same error) goes through a host all-reduce
+ * callback, e.g. torch.distributed over gloo.  Iterations then synchronise
+ * at the exchange and are not graph-captured.  fn returns 0 on success. */
+#define VPB_DT_F64 0
+#define VPB_DT_I64 1
+#define VPB_OP_SUM 0
+#define VPB_OP_MAX 1
+typedef int (*vpb_allreduce_fn)(void *user, void *buf, int64_t count, int32_t dtype, int32_t op);
+int vpb_attach_exchange(vpb_ctx *ctx, int32_t world, int32_t rank, vpb_allreduce_fn fn,
+                        void *user);
 
 /* init phase (vp/core.py:188-196): uniform map (maps.new_uniform), uniform
  * allocation (strat.initial_grid), run_base = 0, history cleared. */

@@ -372,6 +372,25 @@ def gen_integrands():
     out["x3"] = x3
     out["path_integral_d3_xend05"] = lookup("path_integral", dim=3, x_end=0.5,
                                             total_time=2.0).evaluate_batch(x3)
+    # the six Table-2 test functions (vp/integrands.py:106-128) at their
+    # registry dimensions, straight from the reference; drawn after all the
+    # arrays above so those stay unchanged
+    for name in ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff"):
+        spec = lookup(name)
+        x = g.random((4096, spec.dims))
+        x[:3] = [[0.0] * spec.dims, [1.0] * spec.dims, [0.5] * spec.dims]
+        if name == "morokoff":
+            # product underflow (per-axis form), a zero coordinate, off the
+            # unit box (a negative coordinate: NaN in the reference, twice:
+            # an even count), coordinates > 1
+            x[3] = 1e-40
+            x[4, 2] = 0.0
+            x[5, 1] = -0.25
+            x[6, 1] = x[6, 4] = -0.25
+            x[7] = 3.0
+        out[f"x_{name}"] = x
+        with np.errstate(invalid="ignore"):
+            out[name] = spec.evaluate_batch(x)
     save("integrands.npz", **out)
 
 

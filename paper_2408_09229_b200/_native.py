@@ -55,16 +55,24 @@ _c = ctypes
 _P = ctypes.c_void_p
 _I32, _I64, _U64, _F64 = _c.c_int32, _c.c_int64, _c.c_uint64, _c.c_double
 
+# vpb_allreduce_fn (vegas_b200.h): int fn(void *user, void *buf, int64_t count,
+# int32_t dtype, int32_t op) -- the host exchange callback
+ALLREDUCE_FN = _c.CFUNCTYPE(_c.c_int, _P, _P, _I64, _I32, _I32)
+VPB_DT_F64, VPB_DT_I64 = 0, 1
+VPB_OP_SUM, VPB_OP_MAX = 0, 1
+
 # name -> argtypes (all return int status unless listed in _RESTYPES)
 SIGNATURES = {
     "vpb_abi_version": [],
     "vpb_last_error": [],
     "vpb_is_specialised": [_I32, _I32],
+    "vpb_device_count": [_c.POINTER(_I32)],
     "vpb_create": [_c.POINTER(VpbDesc), _c.POINTER(_P)],
     "vpb_destroy": [_P],
     "vpb_nccl_unique_id": [_c.c_char_p],
     "vpb_attach_nccl": [_P, _c.c_char_p, _I32, _I32],
     "vpb_set_shard": [_P, _I32, _I32],
+    "vpb_attach_exchange": [_P, _I32, _I32, ALLREDUCE_FN, _P],
     "vpb_reset": [_P],
     "vpb_iterate": [_P, _I32],
     "vpb_history": [_P, _I32, _P, _P, _P, _c.POINTER(_I32)],

@@ -198,8 +198,12 @@ def _check_bounds(dims, n_intervals, bounds):
 
 
 def _default_device() -> int:
+    """LOCAL_RANK's GPU, modulo the visible devices: launchers that set
+    CUDA_VISIBLE_DEVICES per rank leave every rank one device (ordinal 0)."""
     if "LOCAL_RANK" in os.environ:
-        return int(os.environ["LOCAL_RANK"])
+        n = ctypes.c_int32(0)
+        N.check(N.load().vpb_device_count(ctypes.byref(n)), "vpb_device_count")
+        return int(os.environ["LOCAL_RANK"]) % max(1, n.value)
     return -1
 
 
@@ -211,7 +215,8 @@ class Integrator:
     bench.py and the tests drive it directly to time single iterations."""
 
     def __init__(self, f, bounds, config: IntegratorConfig, *, device: int | None = None,
-                 distributed: bool | None = None, stream: int | None = None):
+                 distributed: bool | None = None, stream: int | None = None,
+                 exchange: str | None = None):
         self.config = config
         self.bounds = [(float(lo), float(hi)) for lo, hi in bounds]
         self.dims = len(self.bounds)
@@ -245,10 +250,11 @@ class Integrator:
         N.check(lib.vpb_create(ctypes.byref(desc), ctypes.byref(ctx)), "vpb_create")
         self._ctx = ctx
         self.world, self.rank = 1, 0
-        self._maybe_distribute(distributed)
+        self._exchange_cb = None
+        self._maybe_distribute(distributed, exchange or os.environ.get("VPB_EXCHANGE", "nccl"))
 
     # -- multi-GPU ------------------------------------------------------------
-    def _maybe_distribute(self, distributed):
+    def _maybe_distribute(self, distributed, exchange="nccl"):
         if distributed is False:
             return
         try:
@@ -264,9 +270,19 @@ class Integrator:
         world, rank = dist.get_world_size(), dist.get_rank()
         if world == 1 and not distributed:
             return
-        from .distributed import nccl_unique_id_broadcast
-        uid = nccl_unique_id_broadcast(self._lib)
-        N.check(self._lib.vpb_attach_nccl(self._ctx, uid, world, rank), "vpb_attach_nccl")
+        if exchange == "host":
+            # the exchange through torch.distributed on host buffers (any
+            # backend, e.g. gloo; ranks may share a GPU) instead of NCCL
+            from .distributed import host_allreduce_callback
+            self._exchange_cb = host_allreduce_callback()
+            N.check(self._lib.vpb_attach_exchange(self._ctx, world, rank, self._exchange_cb,
+                                                  None), "vpb_attach_exchange")
+        elif exchange == "nccl":
+            from .distributed import nccl_unique_id_broadcast
+            uid = nccl_unique_id_broadcast(self._lib)
+            N.check(self._lib.vpb_attach_nccl(self._ctx, uid, world, rank), "vpb_attach_nccl")
+        else:
+            raise ContractViolationError(f"exchange must be 'nccl' or 'host', got {exchange!r}")
         self.world, self.rank = world, rank
 
     # -- iteration control --------------------------------------------------------
@@ -422,7 +438,8 @@ class Integrator:
 
 def integrate(f, bounds, config: IntegratorConfig | None = None, *,
               batched: bool = False, device: int | None = None,
-              distributed: bool | None = None, **overrides) -> IntegralOutcome:
+              distributed: bool | None = None, exchange: str | None = None,
+              **overrides) -> IntegralOutcome:
     """Integrate a registered device integrand over the box given by bounds.
 
     Same contract as vp/core.py:168-238.  ``f`` is a registered integrand
@@ -436,7 +453,8 @@ def integrate(f, bounds, config: IntegratorConfig | None = None, *,
     bounds = [(float(lo), float(hi)) for lo, hi in bounds]
     timing = PhaseTimes()
     t0 = time.perf_counter()
-    integ = Integrator(f, bounds, config, device=device, distributed=distributed)
+    integ = Integrator(f, bounds, config, device=device, distributed=distributed,
+                       exchange=exchange)
     timing.init = time.perf_counter() - t0
     try:
         integ.iterate(config.max_it)

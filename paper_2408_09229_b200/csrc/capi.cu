@@ -261,6 +261,7 @@ struct vpb_ctx {
   bool smem_hist = true;
   bool pairs = false;
   int hs = 1;                  // shared-histogram row stride
+  int hcopies = 1;             // copies of the shared f64 sums
   int layout = 0;              // LAYOUT_* of the fill kernel
   size_t smem = 0;
   // records mode (histograms too large for shared memory): chunked fill ->
@@ -273,9 +274,14 @@ struct vpb_ctx {
   unsigned short *rec_iv = nullptr;
   double *rec_w2 = nullptr, *hw_rec = nullptr;
   unsigned *hc_rec = nullptr;
-  // multi-GPU
+  // multi-GPU: NCCL communicator, or a host all-reduce callback
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  vpb_allreduce_fn exch_fn = nullptr;
+  void *exch_user = nullptr;
+  long long *ctl = nullptr;     // exchange control word [nonfinite, assert, -first failing run]
+  double *hx_f = nullptr;       // pinned host staging (host exchange)
+  long long *hx_i = nullptr;
   // timing
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
@@ -331,6 +337,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.smem_hist = (c->smem_hist || c->rec_k0 > 0) ? 1 : 0;
   a.pairs = c->pairs ? 1 : 0;
   a.hs = c->hs;
+  a.hcopies = c->hcopies;
   a.records = c->records ? 1 : 0;
   a.tile_lo = 0;
   a.tile_hi = (long long)1 << 62;
@@ -369,7 +376,7 @@ int setdev(vpb_ctx *c) {
 int enqueue_plan(vpb_ctx *c, int record, const long long *explicit_rb) {
   plan_scan_kernel<<<1, PLAN_NT, 0, c->st>>>(c->bsum, c->nb, c->sched, c->world, c->rank,
                                              c->h_evals, record, c->ntiles_cap, c->status,
-                                             explicit_rb);
+                                             explicit_rb, c->n_h, c->n_cubes);
   plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,
                                                              c->offsets, c->sched, c->tile_cube,
                                                              c->status);
@@ -390,6 +397,28 @@ int join_side(vpb_ctx *c) {
   CK(cudaEventRecord(c->ev_join, c->side));
   CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
   c->side_open = false;
+  return VPB_OK;
+}
+
+// The exchange through a host all-reduce callback (vpb_attach_exchange):
+// the same three reductions as the NCCL group, staged through pinned host
+// buffers, synchronously (not graph-capturable).
+int host_exchange(vpb_ctx *c) {
+  const size_t m = (size_t)c->dims * c->ng;
+  const size_t nf = m + 2 * (size_t)c->n_cubes;
+  CK(cudaMemcpyAsync(c->hx_f, c->accf, sizeof(double) * nf, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hx_i, c->map_counts, sizeof(long long) * m, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaMemcpyAsync(c->hx_i + m, c->ctl, sizeof(long long) * 3, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->exch_fn(c->exch_user, c->hx_f, (int64_t)nf, VPB_DT_F64, VPB_OP_SUM) != 0 ||
+      c->exch_fn(c->exch_user, c->hx_i, (int64_t)m, VPB_DT_I64, VPB_OP_SUM) != 0 ||
+      c->exch_fn(c->exch_user, c->hx_i + m, 3, VPB_DT_I64, VPB_OP_MAX) != 0)
+    return fail(VPB_ERR_NCCL, "host exchange callback failed");
+  CK(cudaMemcpyAsync(c->accf, c->hx_f, sizeof(double) * nf, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->map_counts, c->hx_i, sizeof(long long) * m, cudaMemcpyHostToDevice,
+                     c->st));
+  CK(cudaMemcpyAsync(c->ctl, c->hx_i + m, sizeof(long long) * 3, cudaMemcpyHostToDevice, c->st));
   return VPB_OK;
 }
 
@@ -450,13 +479,13 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
     const size_t m0 = (size_t)c->rec_k0 * c->ng;   // rows histogrammed by the fill itself
     if (m0 > 0)
       hist_reduce_kernel<<<(unsigned)((m0 + 31) / 32), dim3(32, 8), 0, hs_st>>>(
-          c->hw_part, c->hc_part, c->grid, (long long)m0, c->map_w, c->map_counts);
+          c->hw_part, c->hc_part, c->grid, (long long)m0, c->map_w, c->map_counts, c->status);
     rec_reduce_kernel<<<(unsigned)((m - m0 + 31) / 32), dim3(32, 8), 0, hs_st>>>(
         c->hw_rec, c->hc_rec, c->rec_B, c->dims - c->rec_k0, c->ng, c->map_w + m0,
         c->map_counts + m0, c->status);
   } else if (c->smem_hist) {
     hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, hs_st>>>(
-        c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts);
+        c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts, c->status);
   } else {
     CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, hs_st));
     hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, hs_st>>>(c->hc_glob,
@@ -464,13 +493,25 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
                                                                            c->map_counts);
   }
   CK(cudaGetLastError());
-  if (!defer_join || c->comm) TRY(join_side(c));
-  if (c->comm) {
-    NK(ncclGroupStart());
-    NK(ncclAllReduce(c->accf, c->accf, m + 2 * (size_t)c->n_cubes, ncclFloat64, ncclSum, c->comm,
-                     c->st));
-    NK(ncclAllReduce(c->map_counts, c->map_counts, m, ncclInt64, ncclSum, c->comm, c->st));
-    NK(ncclGroupEnd());
+  const bool exch = c->comm || c->exch_fn;
+  if (!defer_join || exch) TRY(join_side(c));
+  if (exch) {
+    // one exchange per iteration: map_w|s1|s2 (f64 sum), map_counts (i64
+    // sum) and the control word (i64 max: failure flags, first failing run)
+    ctl_pack_kernel<<<1, 1, 0, c->st>>>(c->status, c->err_run, c->ctl);
+    CK(cudaGetLastError());
+    if (c->comm) {
+      NK(ncclGroupStart());
+      NK(ncclAllReduce(c->accf, c->accf, m + 2 * (size_t)c->n_cubes, ncclFloat64, ncclSum,
+                       c->comm, c->st));
+      NK(ncclAllReduce(c->map_counts, c->map_counts, m, ncclInt64, ncclSum, c->comm, c->st));
+      NK(ncclAllReduce(c->ctl, c->ctl, 3, ncclInt64, ncclMax, c->comm, c->st));
+      NK(ncclGroupEnd());
+    } else {
+      TRY(host_exchange(c));
+    }
+    ctl_unpack_kernel<<<1, 1, 0, c->st>>>(c->status, c->err_run, c->ctl);
+    CK(cudaGetLastError());
   }
   return VPB_OK;
 }
@@ -608,7 +649,8 @@ void free_ctx(vpb_ctx *c) {
                   c->pwvals, c->pwterms, c->sched, c->sc, c->h_est, c->h_var, c->h_evals, c->tile_cube,
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
-                  c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec};
+                  c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec,
+                  c->ctl};
   for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
@@ -624,6 +666,8 @@ void free_ctx(vpb_ctx *c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->hx_f) cudaFreeHost(c->hx_f);
+  if (c->hx_i) cudaFreeHost(c->hx_i);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
 
@@ -657,6 +701,15 @@ int vpb_abi_version(void) { return VPB_ABI_VERSION; }
 const char *vpb_last_error(void) { return g_err.c_str(); }
 int vpb_is_specialised(int32_t integrand, int32_t dims) {
   return fill_is_specialised(integrand, dims);
+}
+int vpb_device_count(int32_t *n) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  if (n) *n = c;
+  return VPB_OK;
 }
 
 int vpb_create(const vpb_desc *d, vpb_ctx **out) {
@@ -749,6 +802,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
                            (int)refine_smem_bytes(c->ng)) != cudaSuccess)
     return bail(fail(VPB_ERR_CUDA, "refine smem attribute"));
   A(c->explicit_rb, 1);
+  A(c->ctl, 3);
   // fill geometry: shared histograms when they fit next to the edges
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
@@ -769,13 +823,21 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // the ridge kernels stage the centre table (specialised kernels only)
   const int rc_n = (c->id == VPB_RIDGE && specialisable(c)) ? (int)c->P.p[0] : 0;
   bool fits = false;
-  for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
-    const bool pr = pass < 2 && c->pairs;
-    if (pass < 2 && !c->pairs) continue;
-    const int hs = (pass & 1) ? c->dims : hist_stride(c->dims);
-    const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, pr, hs, rc_n);
-    if (b <= (size_t)optin) { fits = true; c->pairs = pr; c->hs = hs; c->smem = b; }
-  }
+  // VPB_HIST_COPIES=2: two copies of the shared f64 sums (one per half-warp)
+  // when they fit -- fewer same-interval collisions inside a CAS instruction
+  // (measured: cfg4a/b -1.0%, cfg2 -0.7% fill time, cfg1/cfg3 neutral)
+  int want_copies = 2;
+  if (const char *e = std::getenv("VPB_HIST_COPIES")) want_copies = std::atoi(e) == 2 ? 2 : 1;
+  for (int cp = want_copies; cp >= 1 && c->smem_hist && !fits; cp--)
+    for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
+      const bool pr = pass < 2 && c->pairs;
+      if (pass < 2 && !c->pairs) continue;
+      const int hs = (pass & 1) ? c->dims : hist_stride(c->dims);
+      const size_t b = fill_smem_bytes(c->dims, c->ng, c->ns, 1, pr, hs, rc_n, cp);
+      if (b <= (size_t)optin) {
+        fits = true; c->pairs = pr; c->hs = hs; c->smem = b; c->hcopies = cp;
+      }
+    }
   if (!fits) {
     c->smem_hist = false;
     c->pairs = false;
@@ -883,19 +945,14 @@ int vpb_nccl_unique_id(char id_out[128]) {
   return VPB_OK;
 }
 
-// Record chunks for this rank's shard: a shard holds at most
-// ceil(cap / world) runs, so the chunk loop need not walk the whole plan's
-// tile range (tiles are shard-relative).
+// Record chunks per iteration.  A rank's shard is its partition-rule share
+// snapped to hypercube starts, so it can exceed ceil(cap / world) by up to a
+// cube: every rank walks the whole plan's chunk count, and the chunks past
+// its shard end are empty launches (the fill returns before staging the map,
+// the group kernels after one read of the schedule).
 static void shard_chunks(vpb_ctx *c) {
   if (!c->records || c->rec_cap_runs <= 0) return;
-  if (c->world <= 1) {
-    c->n_chunks = (int)((c->rec_cap_runs + c->rec_ch - 1) / c->rec_ch);
-    return;
-  }
-  const long long shard = (c->rec_cap_runs + c->world - 1) / c->world;
-  const long long tiles = (shard + FILL_TILE - 1) / FILL_TILE + 1;
-  const long long tpc = c->rec_ch / FILL_TILE;
-  c->n_chunks = (int)std::max(1ll, (tiles + tpc - 1) / tpc);
+  c->n_chunks = (int)((c->rec_cap_runs + c->rec_ch - 1) / c->rec_ch);
 }
 
 int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank) {
@@ -908,6 +965,7 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
   if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
+  if (c->exch_fn) return fail(VPB_ERR_INVALID, "context already has a host exchange");
   NK(ncclCommInitRank(&c->comm, world, uid, rank));
   c->world = world;
   c->rank = rank;
@@ -922,6 +980,31 @@ int vpb_set_shard(vpb_ctx *c, int32_t world, int32_t rank) {
   shard_chunks(c);
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
   if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  return VPB_OK;
+}
+
+int vpb_attach_exchange(vpb_ctx *c, int32_t world, int32_t rank, vpb_allreduce_fn fn,
+                        void *user) {
+  if (!c || !fn) return fail(VPB_ERR_INVALID, "null context or callback");
+  if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
+  if (c->comm) return fail(VPB_ERR_INVALID, "context already has an NCCL communicator");
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  const size_t m = (size_t)c->dims * c->ng;
+  if (!c->hx_f) {
+    CK(cudaMallocHost(&c->hx_f, sizeof(double) * (m + 2 * (size_t)c->n_cubes)));
+    CK(cudaMallocHost(&c->hx_i, sizeof(long long) * (m + 3)));
+  }
+  // host callbacks cannot live in a captured graph: iterations are enqueued
+  // directly, synchronising at the exchange
+  if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+  if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
+  c->use_graph = false;
+  c->exch_fn = fn;
+  c->exch_user = user;
+  c->world = world;
+  c->rank = rank;
+  shard_chunks(c);
   return VPB_OK;
 }
 
@@ -1552,7 +1635,8 @@ int vpb_build_plan_host(const int64_t *n_h, int64_t n, int64_t *offsets) {
   CK(cudaMemset(sch.p, 0, sizeof(Sched)));
   CK(cudaMemset(rb.p, 0, sizeof(long long)));
   nh_blocksum_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p);
-  plan_scan_kernel<<<1, PLAN_NT>>>(bs.p, nb, sch.p, 1, 0, ev.p, 0, tot / FILL_TILE + 2, st.p, rb.p);
+  plan_scan_kernel<<<1, PLAN_NT>>>(bs.p, nb, sch.p, 1, 0, ev.p, 0, tot / FILL_TILE + 2, st.p, rb.p,
+                                   nh.p, n);
   plan_offsets_kernel<<<(unsigned)nb, PLAN_NT>>>(nh.p, n, bs.p, off.p, sch.p, tc.p, st.p);
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());

@@ -39,6 +39,9 @@ namespace vpb {
 #ifndef VPB_FILL_NT
 #define VPB_FILL_NT 640
 #endif
+#ifndef VPB_HIST_MATCH
+#define VPB_HIST_MATCH 0
+#endif
 #ifndef VPB_FILL_RPT
 #define VPB_FILL_RPT 16   // measured: 8 and 32 lose on cfg1/cfg2 (32: cfg4 -1%, cfg1 +69%)
 #endif
@@ -94,6 +97,7 @@ struct FillArgs {
   double *hw_glob;              // [d*ng] (global-atomic histograms)
   unsigned long long *hc_glob;  // [d*ng]
   int smem_hist;                // 1: CTA-private shared histograms
+  int hcopies;                  // copies of the shared f64 sums (lanes 0-15 / 16-31)
   int records;                  // 1: write (interval, w^2) records for hist_records_kernel
   int dig_bits;                 // bits per packed cube digit (d > 12 kernels)
   long long tile_lo, tile_hi;   // tiles of this launch (records mode: one chunk)
@@ -130,11 +134,11 @@ __host__ __device__ inline int hist_stride(int dims) {
 // shared-memory layout helper (bytes)
 __host__ __device__ inline size_t fill_smem_bytes(int dims, int ng, long long n_strat,
                                                   int smem_hist, int pairs, int hs,
-                                                  int ridge_centres = 0) {
+                                                  int ridge_centres = 0, int hcopies = 1) {
   size_t b = 0;
   if (pairs) b += (size_t)dims * ng * 2 * sizeof(double);              // (E[i], dx[i])
   else b += (size_t)dims * (ng + 1) * sizeof(double);                  // edges
-  if (smem_hist) b += (size_t)hs * ng * (sizeof(double) + sizeof(unsigned));
+  if (smem_hist) b += (size_t)hs * ng * (hcopies * sizeof(double) + sizeof(unsigned));
   b = (b + 15) & ~(size_t)15;
   b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);  // digit/N
   b += (size_t)ridge_centres * sizeof(double);                          // ridge c_i
@@ -236,6 +240,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   // form, bit-identical to integrands.cuh
   constexpr bool GSTREAM = (ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK) && D > 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // records chunks past this rank's shard: nothing to do (grid-uniform)
+  if (a.tile_lo > 0 && a.tile_lo >= a.sched->ntiles) return;
   constexpr int MAXD = D > 0 ? D : VPB_MAX_DIMS;
   const int d = D > 0 ? D : a.dims;
   const int ng = a.ng;
@@ -248,9 +254,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   size_t off = PAIRS ? (size_t)d * ng * sizeof(double2) : (size_t)d * (ng + 1) * sizeof(double);
   double *s_hw = nullptr;
   unsigned *s_hc = nullptr;
+  const int hcopies = (LAYOUT == LAYOUT_RECORDS) ? 1 : a.hcopies;
   if (a.smem_hist) {
     s_hw = reinterpret_cast<double *>(smem_raw + off);
-    off += (size_t)hs * ng * sizeof(double);
+    off += (size_t)hcopies * hs * ng * sizeof(double);
     s_hc = reinterpret_cast<unsigned *>(smem_raw + off);
     off += (size_t)hs * ng * sizeof(unsigned);
   }
@@ -277,8 +284,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   } else {
     for (int i = tid; i < d * (ng + 1); i += NT) s_edges[i] = a.edges[i];
   }
-  if (a.smem_hist)
-    for (int i = tid; i < hs * ng; i += NT) { s_hw[i] = 0.0; s_hc[i] = 0u; }
+  if (a.smem_hist) {
+    for (int i = tid; i < hcopies * hs * ng; i += NT) s_hw[i] = 0.0;
+    for (int i = tid; i < hs * ng; i += NT) s_hc[i] = 0u;
+  }
   if (dq_tab)
     for (int i = tid; i < a.n_strat; i += NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
   if constexpr (RTAB) {
@@ -590,10 +599,37 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
             // the layout changes: the value-returning CAS costs more
             // shared-memory wavefronts than CAST.SPIN, and wavefronts bind.)
             {
+            // two copies of the sums: the half-warps update different copies,
+            // so fewer lanes of one CAS instruction collide on an interval
+            double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
 #pragma unroll
             for (int j = 0; j < (D > 0 ? D : d); j++) {
-              atomicAdd(&s_hw[idx[j]], w2);
+#if VPB_HIST_MATCH
+              // lanes of this warp hitting the same interval: the lowest one
+              // adds the group's w2 (summed in lane order) and count, so the
+              // CAS loop never retries on an intra-warp collision
+              const unsigned act = __activemask();
+              const unsigned grp = __match_any_sync(act, idx[j]);
+              if (grp == (1u << lane)) {
+                atomicAdd(&s_hwl[idx[j]], w2);
+                atomicAdd(&s_hc[idx[j]], 1u);
+              } else {
+                double gs = 0.0;
+                unsigned mm = grp;
+                while (mm) {
+                  const int src = __ffs(mm) - 1;
+                  mm &= mm - 1;
+                  gs = __dadd_rn(gs, __shfl_sync(grp, w2, src));
+                }
+                if (lane == __ffs(grp) - 1) {
+                  atomicAdd(&s_hwl[idx[j]], gs);
+                  atomicAdd(&s_hc[idx[j]], (unsigned)__popc(grp));
+                }
+              }
+#else
+              atomicAdd(&s_hwl[idx[j]], w2);
               atomicAdd(&s_hc[idx[j]], 1u);
+#endif
             }
             }
           } else {
@@ -673,7 +709,9 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
     const bool acc = LAYOUT == LAYOUT_RECORDS && a.tile_lo > 0;
     for (int i = tid; i < nh * ng; i += NT) {   // back to [axis][interval]
       const int j = i / ng, b = i - j * ng;
-      hw[i] = acc ? __dadd_rn(hw[i], s_hw[b * hs + j]) : s_hw[b * hs + j];
+      double v = s_hw[b * hs + j];
+      if (hcopies > 1) v = __dadd_rn(v, s_hw[(size_t)hs * ng + b * hs + j]);
+      hw[i] = acc ? __dadd_rn(hw[i], v) : v;
       hc[i] = acc ? hc[i] + s_hc[b * hs + j] : s_hc[b * hs + j];
     }
   }

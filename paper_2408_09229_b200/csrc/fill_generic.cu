@@ -1,4 +1,6 @@
 // fill_generic.cu -- runtime-dims (D = 0) fill kernels, one per integrand.
+#include <atomic>
+
 #include "fill_launch.h"
 
 namespace vpb {
@@ -6,12 +8,16 @@ namespace vpb {
 namespace {
 template <int ID>
 cudaError_t launch_g(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
-  static bool attr = false;
-  if (!attr) {
+  // the max-dynamic-shared-memory attribute is per device: one bit per ordinal
+  static std::atomic<unsigned long long> attr{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, 0, LAYOUT_RUNTIME>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.fetch_or(bit, std::memory_order_acq_rel);
   }
   fill_kernel<ID, 0, LAYOUT_RUNTIME><<<grid, FILL_NT, smem, st>>>(a);
   return cudaGetLastError();

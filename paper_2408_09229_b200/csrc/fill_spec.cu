@@ -1,6 +1,8 @@
 // fill_spec.cu -- compile-time-dims instantiations of the fused fill kernel
 // for the registry integrands at their registry dimension and the BASELINE
 // configurations (cfg1/3: d=4, cfg2: d=8, cfg4: d=6, cfg5: d=20).
+#include <atomic>
+
 #include "fill_launch.h"
 
 namespace vpb {
@@ -8,12 +10,16 @@ namespace vpb {
 namespace {
 template <int ID, int D, int LAYOUT>
 cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
-  static bool attr = false;
-  if (!attr) {
+  // the max-dynamic-shared-memory attribute is per device: one bit per ordinal
+  static std::atomic<unsigned long long> attr{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.fetch_or(bit, std::memory_order_acq_rel);
   }
   fill_kernel<ID, D, LAYOUT><<<grid, (fill_nt<ID, D, LAYOUT>()), smem, st>>>(a);
   return cudaGetLastError();

@@ -255,11 +255,16 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     // as (prod_j x_j)^(1/d): one pow instead of d (the product's d-1
     // roundings shrink by 1/d under the root; max 8.6e-16 relative from the
     // per-axis form over 3M points, numpy emulation); near underflow of the
-    // product the per-axis form
+    // product the per-axis form; so also for any x_j <= 0 (a zero gives 0, a
+    // negative coordinate NaN, as numpy's x ** (1/d) does) and near overflow
     double px = x[0];
+    bool pos = x[0] > 0.0;
 #pragma unroll
-    for (int j = 1; j < (D > 0 ? D : d); j++) px = __dmul_rn(px, x[j]);
-    if (px >= 1e-280 || px == 0.0) return __dmul_rn(P.p[0], pow(px, P.p[1]));
+    for (int j = 1; j < (D > 0 ? D : d); j++) {
+      px = __dmul_rn(px, x[j]);
+      pos = pos && x[j] > 0.0;
+    }
+    if (pos && px >= 1e-280 && px <= 1e280) return __dmul_rn(P.p[0], pow(px, P.p[1]));
     double prod = pow(x[0], P.p[1]);
 #pragma unroll
     for (int j = 1; j < (D > 0 ? D : d); j++) {

@@ -293,13 +293,52 @@ __device__ __forceinline__ long long block_incl_scan(long long v, long long *wsu
   return v;
 }
 
+// Smallest cube start offsets[h] >= t (t in (0, total)): the rank shards are
+// snapped to hypercube boundaries, so every cube has exactly one owner.
+// Block-wide: bpre = exclusive block prefixes (PLAN_NT cubes per block),
+// n_h the allocation.  Cube starts are strictly increasing (n_h >= 1).
+__device__ long long snap_to_cube(long long t, const long long *bpre, long long nb,
+                                  const long long *n_h, long long n, long long total,
+                                  long long *wsum, long long *s_out) {
+  if (t <= 0) return 0;
+  if (t >= total) return total;
+  if (threadIdx.x == 0) {   // last block whose first cube starts at or before t
+    long long lo = 0, hi = nb - 1;
+    while (lo < hi) {
+      const long long mid = (lo + hi + 1) >> 1;
+      if (bpre[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    s_out[0] = lo;
+    s_out[1] = lo + 1 < nb ? bpre[lo + 1] : total;   // the next block's start
+  }
+  __syncthreads();
+  const long long b = s_out[0];
+  const long long h = b * PLAN_NT + threadIdx.x;
+  const long long v = h < n ? n_h[h] : 0;
+  const long long start = bpre[b] + block_incl_scan(v, wsum) - v;
+  const long long prev_start = (h < n && threadIdx.x > 0) ? start - n_h[h - 1] : start;
+  __syncthreads();
+  // the first cube of the block starting at or after t
+  if (h < n && start >= t && (threadIdx.x == 0 || prev_start < t)) s_out[1] = start;
+  __syncthreads();
+  const long long r = s_out[1];
+  __syncthreads();
+  return r;
+}
+
 // Exclusive scan of the block sums; total; this rank's shard of the run
-// range (vp/executor.py:41-57: the first total % world ranks get +1); run_base
-// bookkeeping (vp/core.py:208) and the evals history.
+// range and run_base bookkeeping (vp/core.py:208) and the evals history.
+// Shards: the reference's partition rule (vp/executor.py:41-57: the first
+// total % world ranks get +1) gives the split points, each snapped forward to
+// the next hypercube start ("sharded by hypercube range"): every cube's runs
+// -- its s1, s2 -- belong to one rank, and the shards stay balanced to
+// within one cube.
 __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, int world, int rank,
                                  long long *hist_evals, int record, long long ntiles_cap,
-                                 int *status, const long long *explicit_run_base) {
+                                 int *status, const long long *explicit_run_base,
+                                 const long long *n_h, long long n_cubes) {
   __shared__ long long wsum[PLAN_NT / 32];
+  __shared__ long long s_snap[2];
   if (*status) return;   // a failed iteration freezes the plan (error reporting)
   long long carry = 0;
   for (long long b0 = 0; b0 < nb; b0 += PLAN_NT) {
@@ -310,8 +349,16 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
     carry += wsum[PLAN_NT / 32 - 1];         // this chunk's total (uniform)
     __syncthreads();                         // wsum reused by the next chunk
   }
+  const long long total = carry;
+  const long long q = total / world, rem = total % world;
+  const long long t0 = rank * q + (rank < rem ? rank : rem);
+  const long long t1 = t0 + q + (rank < rem ? 1 : 0);
+  long long lo = t0, hi = t1;
+  if (world > 1) {
+    lo = snap_to_cube(t0, bsum, nb, n_h, n_cubes, total, wsum, s_snap);
+    hi = snap_to_cube(t1, bsum, nb, n_h, n_cubes, total, wsum, s_snap);
+  }
   if (threadIdx.x == 0) {
-    const long long total = carry;
     Sched s = *sched;
     if (explicit_run_base) {
       s.run_base = *explicit_run_base;
@@ -320,9 +367,8 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
       s.run_base_next = s.run_base + total;
     }
     s.total = total;
-    const long long q = total / world, rem = total % world;
-    s.lo = rank * q + (rank < rem ? rank : rem);
-    s.hi = s.lo + q + (rank < rem ? 1 : 0);
+    s.lo = lo;
+    s.hi = hi;
     s.ntiles = (s.hi - s.lo + FILL_TILE - 1) / FILL_TILE;
     if (s.ntiles > ntiles_cap) { atomicOr(status, 2); s.ntiles = 0; }
     *sched = s;
@@ -386,6 +432,7 @@ __global__ void set_iteration_kernel(Sched *sched, int it) { sched->it = it; }
 // so the result is deterministic (the order differs from a left fold,
 // within the cube-sum tolerance).
 __global__ void fill_fixup_kernel(FillArgs a) {
+  if (*a.status) return;   // failed (now or earlier): the iteration is discarded
   const long long nt = a.sched->ntiles;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -479,9 +526,11 @@ __global__ void fill_fixup_kernel(FillArgs a) {
 // (32 elements x 8 partitions); partition p sums its contiguous range of CTA
 // slices in order, then thread p = 0 adds the 8 partials in order.
 __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
-                                   long long m, double *map_w, long long *map_counts) {
+                                   long long m, double *map_w, long long *map_counts,
+                                   const int *status) {
   __shared__ double sw[8][33];
   __shared__ long long sc[8][33];
+  if (*status) return;   // failed (now or earlier): the iteration is discarded
   const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
   const int p = threadIdx.y;
   const int per = (nparts + 7) / 8;
@@ -517,6 +566,25 @@ __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_par
     map_w[i] = t;
     map_counts[i] = k;
   }
+}
+
+// The exchange's control word, all-reduced with MAX next to the accumulators
+// so that every rank sees every rank's failure (vp/executor.py:151-165: the
+// reference re-raises the lowest failing worker's exception for the whole
+// integration): [non-finite flag, assert flag, -(first failing run)].  The
+// run index is plan-global, so MAX of its negation is the lowest failing run
+// over all ranks; "none" (~0) maps to -INT64_MAX.
+__global__ void ctl_pack_kernel(const int *status, const unsigned long long *err_run,
+                                long long *ctl) {
+  const int st = *status;
+  const unsigned long long e = *err_run;
+  ctl[0] = st & 1;
+  ctl[1] = (st >> 1) & 1;
+  ctl[2] = e == ~0ull ? -0x7FFFFFFFFFFFFFFFll : -(long long)e;
+}
+__global__ void ctl_unpack_kernel(int *status, unsigned long long *err_run, const long long *ctl) {
+  *status |= (int)(ctl[0] | (ctl[1] << 1));
+  *err_run = ctl[2] == -0x7FFFFFFFFFFFFFFFll ? ~0ull : (unsigned long long)(-ctl[2]);
 }
 
 __global__ void hist_glob_convert_kernel(const unsigned long long *hc, long long m,

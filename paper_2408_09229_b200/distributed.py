@@ -24,6 +24,32 @@ def nccl_unique_id_broadcast(lib) -> bytes:
     return obj[0]
 
 
+def host_allreduce_callback():
+    """A vpb_allreduce_fn that all-reduces the library's pinned host staging
+    buffers in place with torch.distributed (the process group's backend,
+    e.g. gloo): the exchange path for ranks without NCCL (tests: several
+    ranks on one GPU).  Keep the returned object alive with the context."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import _native as N
+
+    ops = {N.VPB_OP_SUM: dist.ReduceOp.SUM, N.VPB_OP_MAX: dist.ReduceOp.MAX}
+    types = {N.VPB_DT_F64: ctypes.c_double, N.VPB_DT_I64: ctypes.c_int64}
+
+    def fn(_user, buf, count, dtype, op):
+        try:
+            arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(types[dtype])),
+                                        shape=(int(count),))
+            dist.all_reduce(torch.from_numpy(arr), op=ops[op])   # in place, shares memory
+            return 0
+        except Exception:   # reported by the library as an exchange failure
+            return 1
+
+    return N.ALLREDUCE_FN(fn)
+
+
 def partition_runs(total: int, k: int):
     """vp/executor.py:41-57: k contiguous ranges, the first total % k get +1.
     (The device plan kernel applies the same rule per rank.)"""

@@ -72,3 +72,94 @@ def test_multiprocess_shards_merge_to_whole(world):
     assert kind == "ok", val
     assert val is True
     assert all(p.exitcode == 0 for p in procs)
+
+
+# ----------------------------------------------- the whole iteration, world > 1
+# Every rank runs full iterations (plan -> its hypercube-aligned shard of the
+# fill -> exchange -> replicated update) with the exchange through the host
+# all-reduce callback over gloo (vpb_attach_exchange; the same three
+# reductions as the NCCL group, incl. the control word).
+
+IT_CFG = dict(n_eval=200_000, max_it=4, n_intervals=128, seed=9, batch_size=4096)
+# exponential exp(sum x^2) with the last axis on (0, 30): the top stratum of that
+# axis (x > 26.5) overflows to inf -- its cubes are the last third of the plan, i.e. only the
+# last rank's shard fails (vp/executor.py:119-127)
+NF_BOUNDS = [(0.0, 1.0)] * 9 + [(0.0, 30.0)]
+
+
+def _iterate(bounds, name, distributed):
+    import paper_2408_09229_b200 as P
+    with P.Integrator(name, bounds, P.IntegratorConfig(**IT_CFG), device=0,
+                      distributed=distributed, exchange="host") as it:
+        it.iterate(IT_CFG["max_it"])
+        try:
+            est, var, ev = it.history()
+        except P.NonFiniteIntegrandError as e:
+            return ("nonfinite", [float(v) for v in e.point], float(e.value), int(e.run_index),
+                    it.world, it.rank)
+        return ("ok", est.tolist(), var.tolist(), ev.tolist(), it.edges().tolist(), it.world)
+
+
+def _iter_worker(rank, world, port, case, q):
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        if case == "nonfinite":
+            q.put((rank, _iterate(NF_BOUNDS, "exponential", True)))
+        else:
+            q.put((rank, _iterate([(0.0, 1.0)] * 8, "multipeak8", True)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surfaced to the parent
+        q.put((rank, ("error", f"{type(e).__name__}: {e}")))
+
+
+def _run_ranks(world, case):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + world * 31 + (os.getpid() % 300) + (7 if case == "nonfinite" else 0)
+    procs = [ctx.Process(target=_iter_worker, args=(r, world, port, case, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, res = q.get(timeout=300)
+        out[r] = res
+    for p in procs:
+        p.join(60)
+        if p.is_alive():
+            p.kill()
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_iterations_match_single(world):
+    out = _run_ranks(world, "ok")
+    single = _iterate([(0.0, 1.0)] * 8, "multipeak8", False)
+    assert single[0] == "ok"
+    for r in range(world):
+        kind, est, var, ev, edges, w = out[r]
+        assert kind == "ok" and w == world, out[r]
+        assert ev == single[3]                              # plan.total per iteration, exact
+        np.testing.assert_allclose(est, single[1], rtol=1e-10)
+        np.testing.assert_allclose(var, single[2], rtol=1e-8)
+        np.testing.assert_allclose(edges, single[4], rtol=1e-12, atol=0)
+        # the replicated update leaves every rank with the same map, bitwise
+        assert edges == out[0][4]
+
+
+def test_multiprocess_nonfinite_raises_on_every_rank():
+    # only the last rank's shard evaluates to inf; every rank must raise the
+    # same NonFiniteIntegrandError (the lowest failing run of the iteration,
+    # its point and value) as the single-process run
+    out = _run_ranks(2, "nonfinite")
+    single = _iterate(NF_BOUNDS, "exponential", False)
+    assert single[0] == "nonfinite"
+    for r in range(2):
+        assert out[r][0] == "nonfinite", out[r]
+        assert out[r][1:4] == single[1:4], (out[r], single)
+        assert out[r][4:] == (2, r)

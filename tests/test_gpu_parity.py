@@ -162,6 +162,16 @@ def test_application_integrand_values(golden):
         np.testing.assert_allclose(v, g[key], rtol=1e-12, atol=atol, err_msg=key)
 
 
+def test_table2_integrand_values(golden):
+    # the six Table-2 test functions (vp/integrands.py:106-128) against the
+    # reference's own values, incl. Morokoff's per-axis fallback (product
+    # underflow, a zero / negative coordinate: NaN like numpy's x ** (1/d))
+    g = golden("integrands.npz")
+    for name in ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff"):
+        v = P.lookup(name).evaluate_batch(g[f"x_{name}"])
+        np.testing.assert_allclose(v, g[name], rtol=1e-13, atol=1e-300, err_msg=name)
+
+
 def test_registry_reference_integrands_match_oracle():
     g = np.random.default_rng(7)
     for name in ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff"):

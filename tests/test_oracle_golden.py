@@ -131,6 +131,17 @@ def test_integrand_values(golden):
         np.testing.assert_allclose(v, g[name], rtol=2e-13, atol=atol, err_msg=name)
 
 
+def test_table2_integrands(golden):
+    # vp/integrands.py:106-128 (sinexp, linear, cosine, exponential,
+    # roos_arnold, morokoff) against values from the reference itself
+    g = golden("integrands.npz")
+    for name in ("sinexp", "linear", "cosine", "exponential", "roos_arnold", "morokoff"):
+        x = g[f"x_{name}"]
+        with np.errstate(invalid="ignore"):
+            v = O.evaluate(name, x)
+        np.testing.assert_allclose(v, g[name], rtol=1e-13, atol=1e-300, err_msg=name)
+
+
 def test_application_integrands(golden):
     # vp/integrands.py:196-251 (asian_option via erfinv, path_integral), default
     # and non-default parameters, against values from the reference itself.
