@@ -332,7 +332,8 @@ class Integrator:
         return a.value, k.value
 
     _LAYOUTS = {0: "edge rows + shared histograms", 1: "pair table + shared histograms",
-                2: "records + per-group shared histograms", 3: "generic runtime-dims kernel"}
+                2: "records + per-group shared histograms", 3: "generic runtime-dims kernel",
+                4: "split: 2-CTA clusters, half the axes' map rows and histograms per SM"}
 
     def fill_layout(self) -> dict:
         """The fill's shared-memory layout, record chunks per iteration and

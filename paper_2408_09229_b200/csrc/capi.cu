@@ -258,6 +258,8 @@ struct vpb_ctx {
   long long *explicit_rb = nullptr;
   // fill launch geometry
   int grid = 0;
+  int grid_tiles = 0;          // tile walkers (CTAs, or 2-CTA clusters for the split fill)
+  bool split = false;          // LAYOUT_SPLIT
   bool smem_hist = true;
   bool pairs = false;
   int hs = 1;                  // shared-histogram row stride
@@ -318,7 +320,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.seed = c->seed;
   a.keys = PhiloxKeys(c->seed);
   a.nsdiv = MagicDiv((uint32_t)c->ns);
-  const unsigned long long step = (unsigned long long)c->grid * FILL_TILE;
+  const unsigned long long step = (unsigned long long)c->grid_tiles * FILL_TILE;
   a.dk = (long long)(step / (unsigned long long)c->batch);
   a.ds = (long long)(step % (unsigned long long)c->batch);
   a.sched = c->sched;
@@ -438,7 +440,9 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   FillArgs a = fill_args(c);
   if (timed) CK(cudaEventRecord(c->f0, c->st));
   if (k0) CK(rec_event(c, k0));
-  if (!c->records) {
+  if (c->split) {
+    CK(launch_fill_split(c->id, c->dims, c->grid, c->smem, c->st, a));
+  } else if (!c->records) {
     CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
   } else {
     // chunks of rec_ch runs: fill (records) -> per-group shared histograms
@@ -485,7 +489,8 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
         c->map_counts + m0, c->status);
   } else if (c->smem_hist) {
     hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, hs_st>>>(
-        c->hw_part, c->hc_part, c->grid, (long long)m, c->map_w, c->map_counts, c->status);
+        c->hw_part, c->hc_part, c->grid_tiles, (long long)m, c->map_w, c->map_counts,
+        c->status);
   } else {
     CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, hs_st));
     hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, hs_st>>>(c->hc_glob,
@@ -811,7 +816,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // layouts in order of preference: pair table + shared histograms (compiled
   // (id, dims) only), edge rows + shared histograms, edge rows + global
   // histograms
-  // VPB_FILL_LAYOUT=records|global|edges forces a layout (tests, A/B)
+  // VPB_FILL_LAYOUT=records|global|edges|split forces a layout (tests, A/B)
   const char *force = std::getenv("VPB_FILL_LAYOUT");
   const std::string forced = force ? force : "";
   c->smem_hist = forced != "records" && forced != "global";
@@ -843,14 +848,32 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     c->pairs = false;
     c->smem = fill_smem_bytes(c->dims, c->ng, c->ns, 0, 0, 0, rc_n);
   }
+  // histograms too large for one SM's shared memory: the split fill (2-CTA
+  // clusters, half the axes and their histograms per CTA) where compiled
+  // (VPB_NO_SPLIT / VPB_FILL_LAYOUT=records|global switch it off), else
+  // records mode (chunked fill + shared-memory histograms per 8-axis group),
+  // else global atomics
+  if ((!fits || forced == "split") && forced != "records" && forced != "global" &&
+      forced != "edges" &&
+      !std::getenv("VPB_NO_SPLIT") && fill_has_split(c->id, c->dims) &&
+      specialisable(c)) {
+    const size_t b =
+        fill_split_smem_bytes(c->dims, c->ng, c->ns, fill_split_nt(c->id, c->dims), 1);
+    if (b <= (size_t)optin) {
+      c->split = true;
+      c->smem_hist = true;
+      c->hs = c->dims / 2;
+      c->hcopies = 1;
+      c->smem = b;
+    }
+  }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
-  // histograms too large for shared memory: records mode (chunked fill +
-  // shared-memory histograms per 8-axis group), else global atomics
   c->records = !c->smem_hist && forced != "global" && c->ng <= 65535 &&
                hist_records_smem(c->ng) <= (size_t)optin;
   const bool spec = specialisable(c);
-  const int layout = (c->records && spec)     ? LAYOUT_RECORDS
+  const int layout = c->split                 ? LAYOUT_SPLIT
+                     : (c->records && spec)   ? LAYOUT_RECORDS
                      : c->pairs               ? LAYOUT_PAIRS
                      : (c->smem_hist && spec) ? LAYOUT_EDGES
                                               : LAYOUT_RUNTIME;
@@ -864,10 +887,19 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     c->hs = REC_K0;
     c->smem = b;
   }
-  int per_sm = 0;
-  if (fill_occupancy(c->id, c->dims, layout, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
-    return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
-  c->grid = sms * per_sm;
+  if (c->split) {
+    int clusters = 0;
+    if (fill_split_clusters(c->id, c->dims, c->smem, &clusters) != cudaSuccess || clusters < 1)
+      return bail(fail(VPB_ERR_CUDA, "split fill kernel cannot be resident"));
+    c->grid = 2 * clusters;
+    c->grid_tiles = clusters;
+  } else {
+    int per_sm = 0;
+    if (fill_occupancy(c->id, c->dims, layout, c->smem, &per_sm) != cudaSuccess || per_sm < 1)
+      return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
+    c->grid = sms * per_sm;
+    c->grid_tiles = c->grid;
+  }
   if (c->records) {
     c->n_groups = (c->dims - c->rec_k0 + 7) / 8;
     const long long cap_runs = c->ntiles_cap * FILL_TILE;
@@ -906,8 +938,8 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
       A(c->hc_part, (size_t)c->grid * c->rec_k0 * c->ng);
     }
   } else if (c->smem_hist) {
-    A(c->hw_part, (size_t)c->grid * m);
-    A(c->hc_part, (size_t)c->grid * m);
+    A(c->hw_part, (size_t)c->grid_tiles * m);   // one slice per CTA (SPLIT: per cluster)
+    A(c->hc_part, (size_t)c->grid_tiles * m);
   } else {
     A(c->hw_glob, m);
     A(c->hc_glob, m);

@@ -31,6 +31,7 @@
 #pragma once
 #include <cstdint>
 
+#include "cluster.cuh"
 #include "devmath.cuh"
 #include "integrands.cuh"
 
@@ -156,6 +157,31 @@ constexpr int LAYOUT_EDGES = 0;     // edge rows + shared histograms
 constexpr int LAYOUT_PAIRS = 1;     // pair table + shared histograms
 constexpr int LAYOUT_RECORDS = 2;   // edge rows + records (hist.cuh)
 constexpr int LAYOUT_RUNTIME = 3;   // generic kernel: a.smem_hist / a.records / global atomics
+// SPLIT (many axes, separable integrand: the d = 20 Gaussian of cfg5): a
+// cluster of two CTAs (two SMs) processes the same runs; CTA c samples axes
+// [c d/2, (c+1) d/2) with their map rows and interval histograms in its own
+// shared memory, and the pair swaps one (partial sum of (x_j - mu)^2, partial
+// Jacobian) per run through distributed shared memory -- so d * ng
+// histograms twice the size of one SM's shared memory stay on chip (no
+// records through HBM).  Both CTAs combine the partials with the same
+// commutative IEEE ops, i.e. get bit-identical f, jf and w2; CTA 0 keeps the
+// cube sums.
+constexpr int LAYOUT_SPLIT = 4;
+
+// shared memory of the split layout (per CTA): map rows and histograms of d/2
+// axes, digit table, double-buffered exchange slots and their mbarriers
+__host__ __device__ inline size_t fill_split_smem_bytes(int dims, int ng, long long n_strat,
+                                                        int nt, int hcopies = 1) {
+  const int h = dims / 2;
+  size_t b = (size_t)h * (ng + 1) * sizeof(double);
+  b += (size_t)h * ng * (hcopies * sizeof(double) + sizeof(unsigned));
+  b = (b + 15) & ~(size_t)15;
+  b += (n_strat <= DQ_TABLE_MAX ? (size_t)n_strat : 0) * sizeof(double);
+  b = (b + 16 + 15) & ~(size_t)15;                   // block flags
+  b += (size_t)2 * (nt / 32) * 32 * 16;              // exchange slots [2][warps][32] double2
+  b += (size_t)2 * (nt / 32) * 8;                    // their mbarriers
+  return b;
+}
 
 // Integrands whose value does not depend on the order of the axes (up to the
 // rounding of their sums/products): the fill may hand them the coordinates
@@ -186,6 +212,9 @@ __host__ __device__ constexpr bool axis_symmetric() {
 #ifndef VPB_REC_NT
 #define VPB_REC_NT VPB_STREAM_NT
 #endif
+#ifndef VPB_SPLIT_NT
+#define VPB_SPLIT_NT 768   // at most 768: the exchange slots grow with the warps
+#endif
 #ifndef VPB_TABLE_RIDGE
 #define VPB_TABLE_RIDGE 1   // cfg3 -0.4%
 #endif
@@ -199,7 +228,8 @@ __host__ __device__ constexpr bool dq_from_table() {
 
 template <int ID, int D, int LAYOUT>
 __host__ __device__ constexpr int fill_nt() {
-  return dq_from_table<ID, D>()                      ? VPB_TABLE_NT
+  return (LAYOUT == LAYOUT_SPLIT)                    ? VPB_SPLIT_NT
+         : dq_from_table<ID, D>()                    ? VPB_TABLE_NT
          : (LAYOUT == LAYOUT_RECORDS && D > 12)      ? VPB_REC_NT
          : ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
              ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) &&
@@ -211,6 +241,13 @@ template <int ID, int D, int LAYOUT>
 __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(const FillArgs a) {
   constexpr int NT = fill_nt<ID, D, LAYOUT>();
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
+  constexpr bool SPLIT = LAYOUT == LAYOUT_SPLIT;
+  static_assert(!SPLIT || (ID == VPB_GAUSSIAN && D > 0 && D % 2 == 0),
+                "split fill: the Gaussian at even d");
+  constexpr int HX = SPLIT ? D / 2 : D;     // axes this CTA samples (SPLIT: half)
+  const unsigned crank = SPLIT ? cluster_ctarank() : 0u;
+  const unsigned partner = crank ^ 1u;
+  const int ax0 = SPLIT ? (int)crank * HX : 0;   // first axis of this CTA
   // records layout with many axes: the first K0 axes are histogrammed in this
   // kernel's spare shared memory (next to the edges), the rest go to records
   constexpr int K0 = (LAYOUT == LAYOUT_RECORDS && D >= 12) ? REC_K0 : 0;
@@ -251,7 +288,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   // ---- shared memory carve-up
   double *s_edges = reinterpret_cast<double *>(smem_raw);
   double2 *s_pair = reinterpret_cast<double2 *>(smem_raw);
-  size_t off = PAIRS ? (size_t)d * ng * sizeof(double2) : (size_t)d * (ng + 1) * sizeof(double);
+  size_t off = PAIRS ? (size_t)d * ng * sizeof(double2)
+                     : (size_t)(SPLIT ? HX : d) * (ng + 1) * sizeof(double);
   double *s_hw = nullptr;
   unsigned *s_hc = nullptr;
   const int hcopies = (LAYOUT == LAYOUT_RECORDS) ? 1 : a.hcopies;
@@ -273,6 +311,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   const int dbits = a.dig_bits;                 // bits per packed digit (!DQ_REG)
   const uint64_t dmask = (1ull << dbits) - 1;
   int *s_flag = reinterpret_cast<int *>(smem_raw + off);
+  off = (off + 16 + 15) & ~(size_t)15;
+  double2 *s_x = reinterpret_cast<double2 *>(smem_raw + off);   // SPLIT exchange slots
+  off += SPLIT ? (size_t)2 * (NT / 32) * 32 * sizeof(double2) : 0;
+  uint64_t *s_bar = reinterpret_cast<uint64_t *>(smem_raw + off);
 
   if constexpr (PAIRS) {
     for (int i = tid; i < d * ng; i += NT) {
@@ -281,6 +323,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
       // [axis][interval], or [interval][axis] for XPERM
       s_pair[XPERM ? b * D + j : i] = make_double2(lo, __dadd_rn(a.edges[j * (ng + 1) + b + 1], -lo));
     }
+  } else if constexpr (SPLIT) {   // this CTA's map rows
+    for (int i = tid; i < HX * (ng + 1); i += NT) s_edges[i] = a.edges[(size_t)ax0 * (ng + 1) + i];
   } else {
     for (int i = tid; i < d * (ng + 1); i += NT) s_edges[i] = a.edges[i];
   }
@@ -296,13 +340,25 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   }
 
   if (tid == 0) s_flag[0] = *a.status;   // an earlier iteration failed: nothing to fill
+  if constexpr (SPLIT) {
+    if (tid < 2 * (NT / 32)) {
+      mbar_init(smem_u32(s_bar + tid), 1);
+      fence_mbar_init_cluster();
+    }
+  }
   const Sched S = *a.sched;
   const PhiloxKeys &K = a.keys;
   const long long lo = S.lo, hi = S.hi, ntiles = S.ntiles;
   const unsigned long long batch = (unsigned long long)a.batch;
   const unsigned long long stride_half = (unsigned long long)((d + (d & 1)) >> 1);
   __syncthreads();
-  if (s_flag[0]) return;   // block-uniform
+  int stop = s_flag[0];
+  if constexpr (SPLIT) {   // barriers visible to the partner; the pair takes CTA 0's flag
+    cluster_sync_all();
+    stop = ld_dsmem_s32(mapa_u32(smem_u32(s_flag), 0));
+    cluster_sync_all();
+  }
+  if (stop) return;   // block-uniform (cluster-uniform for SPLIT)
 
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
@@ -312,15 +368,33 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   // [L, U) = the launch's tile range
   const long long tL = a.tile_lo, tU = min(a.tile_hi, ntiles);
   const long long P = (tU - tL + NW - 1) / NW;
-  const long long t_beg = tL + (long long)warp * P + blockIdx.x;
+  // SPLIT: the two CTAs of a cluster walk the same tiles
+  const long long cid = SPLIT ? (long long)(blockIdx.x >> 1) : (long long)blockIdx.x;
+  const long long ncl = SPLIT ? (long long)(gridDim.x >> 1) : (long long)gridDim.x;
+  const long long t_beg = tL + (long long)warp * P + cid;
   const long long t_end = min(tL + (long long)(warp + 1) * P, tU);
   const long long rec0 = lo + tL * FILL_TILE;   // run of record 0 (records mode)
   // (k, slot) of this lane's first run in its first tile; advanced per grid stride
   unsigned long long g0 = (unsigned long long)(S.run_base + lo + t_beg * FILL_TILE +
                                                (long long)lane * FILL_RPT);
   unsigned long long kk = g0 / batch, slot = g0 % batch;
+  // SPLIT: one swap of per-run partials with the partner CTA's same lane
+  // (slot = step parity; the same number of steps in both CTAs)
+  unsigned xstep = 0;
+  auto pair_xchg = [&](double u, double v) -> double2 {
+    const int slot_ = (int)(xstep & 1u);
+    const unsigned par = (xstep >> 1) & 1u;
+    xstep++;
+    const int bi = slot_ * (NT / 32) + (tid >> 5);
+    const uint32_t lbar = smem_u32(s_bar + bi);
+    const uint32_t lbuf = smem_u32(s_x + bi * 32 + (tid & 31));
+    st_async_f64x2(mapa_u32(lbuf, partner), u, v, mapa_u32(lbar, partner));
+    if ((tid & 31) == 0) mbar_arrive_expect_tx(lbar, 32 * 16);
+    mbar_wait_parity(lbar, par);
+    return s_x[bi * 32 + (tid & 31)];
+  };
 
-  for (long long tile = t_beg; tile < t_end; tile += gridDim.x) {
+  for (long long tile = t_beg; tile < t_end; tile += ncl) {
     const long long T0 = lo + tile * FILL_TILE;
     const long long T1 = min(T0 + (long long)FILL_TILE, hi);
     const long long c_first = a.tile_cube[tile];
@@ -332,6 +406,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
     const long long r1 = min(r0 + (long long)FILL_RPT, T1);
     SegItem H{-1, 0.0, 0.0}, T{-1, 0.0, 0.0};
     int t_through = 0;
+    // SPLIT: every lane takes part in lane 0's number of swaps
+    const int nsteps = (int)min((long long)FILL_RPT, T1 - T0);
 
     if (r0 < r1) {
       // cube of r0: largest i with win[i] <= r0
@@ -393,8 +469,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         const bool before = cb < seg_beg;   // cube started before this lane
         const bool after = ce > seg_end;    // cube continues past this lane
         if (!before && !after) {
-          a.s1[cube] = v1;
-          a.s2[cube] = v2;
+          if (!SPLIT || crank == 0) {
+            a.s1[cube] = v1;
+            a.s2[cube] = v2;
+          }
         } else if (before && !after) {
           H = {cube, v1, v2};
         } else {
@@ -417,7 +495,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
           load_digits(cube);
         }
         // ---- sample (vp/kernels.py:59-88)
-        StreamSum<STREAM ? D : 1> gacc[NPK > 0 ? NPK : 1];
+        StreamSum<STREAM ? HX : 1> gacc[NPK > 0 ? NPK : 1];
         double gz = ID == VPB_GENZ_PRODUCTPEAK ? 1.0 : 0.0;   // GSTREAM running value
         auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
           if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {   // s += x_j a_j
@@ -434,11 +512,25 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
             }
           }
         };
-        double x[MAXD];
-        int iv[MAXD];
+        double x[SPLIT ? HX : MAXD];
+        int iv[SPLIT ? HX : MAXD];
         double jac = 1.0;
         uint64_t w0 = 0, w1 = 0;
-        if constexpr (XPERM) {
+        if constexpr (SPLIT) {
+#pragma unroll
+          for (int jl = 0; jl < HX; jl++) {   // axes ax0 + jl (ax0 even: same Philox pairs)
+            const int j = ax0 + jl;
+            if ((jl & 1) == 0) {
+              const unsigned long long blk = base + (unsigned long long)(j >> 1);
+              philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+                     w0, w1);
+            }
+            x[jl] = sample_axis((jl & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
+                                EdgeRow{s_edges + jl * (ng + 1)}, jac, iv[jl]);
+            const double u = __dadd_rn(x[jl], -a.P.p[0]);   // (x_j - mu)^2, this half
+            gacc[0].add(jl, __dmul_rn(u, u));
+          }
+        } else if constexpr (XPERM) {
 #pragma unroll
           for (int k2 = 0; k2 < D / 2; k2++) {
             const unsigned long long blk = base + (unsigned long long)(k2 ^ (xr >> 1));
@@ -491,9 +583,19 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         }
         }   // !XPERM
         // ---- integrand (f_batch), finiteness (vp/executor.py:119-127)
+        double gsum = 0.0;
+        if constexpr (SPLIT) {
+          // swap (partial sum, partial Jacobian) with the partner; a + b and
+          // a * b are commutative in IEEE arithmetic, so both CTAs get the same bits
+          const double2 o = pair_xchg(gacc[0].result(), jac);
+          gsum = __dadd_rn(gacc[0].result(), o.x);
+          jac = __dmul_rn(jac, o.y);
+        } else if constexpr (STREAM) {
+          gsum = gacc[0].result();
+        }
         double f;
         if constexpr (STREAM && NPK == 1) {   // integrands.cuh VPB_GAUSSIAN, streamed sum
-          f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gacc[0].result(), a.P.p[3], a.P.p[4])));
+          f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gsum, a.P.p[3], a.P.p[4])));
         } else if constexpr (STREAM) {        // VPB_MULTIPEAK with 3 peaks (host-checked)
           double e[NPK];
 #pragma unroll
@@ -563,6 +665,27 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
               }
               *reinterpret_cast<uint4 *>(a.rec_iv + ((size_t)g * a.rec_ch + ri) * 8) =
                   make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          } else if constexpr (SPLIT) {
+            // this CTA's axes, lane-rotated (barrel rotation by lane % HX)
+            const int rot = lane % HX;
+            int idx[HX];
+#pragma unroll
+            for (int jl = 0; jl < HX; jl++) idx[jl] = iv[jl] * hs + jl;
+#pragma unroll
+            for (int b = 1; b < HX; b <<= 1) {
+              const bool on = (rot & b) != 0;
+              int t[HX];
+#pragma unroll
+              for (int jl = 0; jl < HX; jl++) t[jl] = on ? idx[(jl + b) % HX] : idx[jl];
+#pragma unroll
+              for (int jl = 0; jl < HX; jl++) idx[jl] = t[jl];
+            }
+            double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
+#pragma unroll
+            for (int jl = 0; jl < HX; jl++) {
+              atomicAdd(&s_hwl[idx[jl]], w2);
+              atomicAdd(&s_hc[idx[jl]], 1u);
             }
           } else if (!RT || a.smem_hist) {
             // Lane-rotated dimension order: at step s lane l updates dim
@@ -643,6 +766,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
         if (++sl == batch) { sl = 0; base += stride_half; }
       }
       close_segment(n);
+      if constexpr (SPLIT)   // lane 0's remaining swaps (fewer runs in the tile's end)
+        for (int rr = n; rr < nsteps; rr++) pair_xchg(0.0, 1.0);
+    } else if constexpr (SPLIT) {
+      for (int rr = 0; rr < nsteps; rr++) pair_xchg(0.0, 1.0);
     }
 
     // ---- warp segmented scan of the tail items (chain values flow forward)
@@ -668,22 +795,25 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
     if (H.key >= 0) {
       if (lane > 0) { h1 = __dadd_rn(pe1, H.v1); h2 = __dadd_rn(pe2, H.v2); }
       if (lane > 0 && pfl) {
-        a.s1[H.key] = h1;
-        a.s2[H.key] = h2;
+        if (!SPLIT || crank == 0) {
+          a.s1[H.key] = h1;
+          a.s2[H.key] = h2;
+        }
       } else {
         head_carry = true;
       }
     }
+    if (SPLIT && crank != 0) head_carry = false;   // CTA 0 keeps the cube sums
     if (head_carry) {
       a.ck_head[tile] = H.key;
       a.cv_head[2 * tile] = h1;
       a.cv_head[2 * tile + 1] = h2;
     }
     const unsigned any_head = __ballot_sync(0xffffffffu, head_carry);
-    if (lane == 0 && any_head == 0) a.ck_head[tile] = -1;
+    if (lane == 0 && any_head == 0 && (!SPLIT || crank == 0)) a.ck_head[tile] = -1;
     // ---- the tile's last lane with runs publishes the tail carry
     const int last = (int)((T1 - T0 + FILL_RPT - 1) / FILL_RPT) - 1;
-    if (lane == last) {
+    if (lane == last && (!SPLIT || crank == 0)) {
       if (T.key >= 0) {
         a.ck_tail[tile] = T.key;
         a.cv_tail[2 * tile] = e1;
@@ -702,9 +832,12 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
 
   if (a.smem_hist) {
     __syncthreads();
-    const int nh = LAYOUT == LAYOUT_RECORDS ? K0 : d;   // axes histogrammed here
-    double *hw = a.hw_part + (size_t)blockIdx.x * nh * ng;
-    unsigned *hc = a.hc_part + (size_t)blockIdx.x * nh * ng;
+    const int nh = LAYOUT == LAYOUT_RECORDS ? K0 : (SPLIT ? HX : d);   // axes histogrammed here
+    // SPLIT: rows [ax0, ax0 + HX) of the cluster's slice
+    double *hw = a.hw_part + (SPLIT ? (size_t)cid * d * ng + (size_t)ax0 * ng
+                                    : (size_t)blockIdx.x * nh * ng);
+    unsigned *hc = a.hc_part + (SPLIT ? (size_t)cid * d * ng + (size_t)ax0 * ng
+                                      : (size_t)blockIdx.x * nh * ng);
     // records layout: the chunks of an iteration add into the CTA's slice
     const bool acc = LAYOUT == LAYOUT_RECORDS && a.tile_lo > 0;
     for (int i = tid; i < nh * ng; i += NT) {   // back to [axis][interval]
@@ -715,6 +848,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
       hc[i] = acc ? hc[i] + s_hc[b * hs + j] : s_hc[b * hs + j];
     }
   }
+  if constexpr (SPLIT) cluster_sync_all();   // no CTA leaves while its partner may still write
 }
 
 }  // namespace vpb

@@ -18,6 +18,15 @@ cudaError_t fill_occupancy(int id, int dims, int layout, size_t smem, int *ctas_
 // 1 if (id, dims) has a compile-time specialisation.
 int fill_is_specialised(int id, int dims);
 
+// The split fill (LAYOUT_SPLIT: 2-CTA clusters, half the axes per CTA) for
+// (id, dims) if compiled; its launch (cluster dims 2) and the clusters that
+// can be resident at once with `smem` bytes per CTA.
+int fill_has_split(int id, int dims);
+cudaError_t launch_fill_split(int id, int dims, int grid, size_t smem, cudaStream_t st,
+                              const FillArgs &a);
+cudaError_t fill_split_clusters(int id, int dims, size_t smem, int *clusters);
+int fill_split_nt(int id, int dims);
+
 // generic kernels (fill_generic.cu)
 cudaError_t launch_fill_generic(int id, int grid, size_t smem, cudaStream_t st,
                                 const FillArgs &a);

@@ -71,6 +71,83 @@ cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st
   return launch_fill_generic(id, grid, smem, st, a);   // incl. global-atomic histograms
 }
 
+// ---- split (2-CTA cluster) kernels
+#define VPB_SPLIT_LIST(X) X(VPB_GAUSSIAN, 20)
+
+namespace {
+template <int ID, int D>
+cudaLaunchConfig_t split_config(int grid, size_t smem, cudaStream_t st,
+                                cudaLaunchAttribute *attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)fill_nt<ID, D, LAYOUT_SPLIT>());
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+template <int ID, int D>
+cudaError_t split_attr() {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT_SPLIT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return cudaSuccess;
+}
+template <int ID, int D>
+cudaError_t launch_split_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
+  cudaError_t e = split_attr<ID, D>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = split_config<ID, D>(grid, smem, st, attr);
+  return cudaLaunchKernelEx(&cfg, fill_kernel<ID, D, LAYOUT_SPLIT>, a);
+}
+template <int ID, int D>
+cudaError_t split_clusters_one(size_t smem, int *clusters) {
+  cudaError_t e = split_attr<ID, D>();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = split_config<ID, D>(2, smem, nullptr, attr);
+  return cudaOccupancyMaxActiveClusters(clusters, fill_kernel<ID, D, LAYOUT_SPLIT>, &cfg);
+}
+}  // namespace
+
+int fill_has_split(int id, int dims) {
+#define X(I, D) if (id == I && dims == D) return 1;
+  VPB_SPLIT_LIST(X)
+#undef X
+  return 0;
+}
+int fill_split_nt(int id, int dims) {
+#define X(I, D) if (id == I && dims == D) return fill_nt<I, D, LAYOUT_SPLIT>();
+  VPB_SPLIT_LIST(X)
+#undef X
+  return 0;
+}
+cudaError_t launch_fill_split(int id, int dims, int grid, size_t smem, cudaStream_t st,
+                              const FillArgs &a) {
+#define X(I, D) if (id == I && dims == D) return launch_split_one<I, D>(grid, smem, st, a);
+  VPB_SPLIT_LIST(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+cudaError_t fill_split_clusters(int id, int dims, size_t smem, int *clusters) {
+#define X(I, D) if (id == I && dims == D) return split_clusters_one<I, D>(smem, clusters);
+  VPB_SPLIT_LIST(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t fill_occupancy(int id, int dims, int layout, size_t smem, int *ctas) {
 #define X(I, D)                                                                  \
   if (id == I && dims == D && layout != LAYOUT_RUNTIME) {                        \

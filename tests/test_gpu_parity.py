@@ -9,6 +9,8 @@ Bars (BASELINE.json north_star):
     sums in a different, but fixed, order; integrand exp differs by ulps)
   * grid edges: rtol 1e-12; integral: per-iteration |dI| well inside 3 sigma
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -215,7 +217,7 @@ def test_fill_matches_oracle(name, dims, ng, ns, nh):
     edges[:, 0], edges[:, -1] = 0.0, 1.0
     seed, batch, rb = 12345, 1 << 20, 987654321
     got = ops.parallel_fill(off, edges, ns, seed, batch, name, run_base=rb)
-    ref = O.fill(off, edges, ns, seed, batch, rb, name)
+    ref = O.fill(off, edges, ns, seed, batch, rb, name, workers=os.cpu_count() or 1)
     np.testing.assert_array_equal(got[1], ref[1])   # map counts
     np.testing.assert_array_equal(got[4], ref[4])   # cube counts
     # the Asian payoff max(S - K, 0) cancels near the strike (device vs libm
@@ -278,6 +280,19 @@ def test_fill_layouts_match_oracle(monkeypatch, layout, chunk, name, dims, ng, n
     test_fill_matches_oracle(name, dims, ng, ns, nh)
 
 
+@pytest.mark.parametrize("name,dims,ng,ns,nh", [
+    ("gaussian20", 20, 64, 1, (5000, 5001)),       # one cube spanning many tiles
+    ("gaussian20", 20, 1024, 2, (2, 40)),           # cfg5 geometry: 2^20 cubes
+    ("gaussian20", 20, 1024, 2, (150, 250)),        # ~2e8 runs, many tiles per warp
+])
+def test_fill_split_matches_oracle(monkeypatch, name, dims, ng, ns, nh):
+    # the split fill (2-CTA clusters: half the axes per CTA, per-run partials
+    # swapped through distributed shared memory) against the oracle, incl.
+    # partial tiles and lanes without runs at the shard end
+    monkeypatch.setenv("VPB_FILL_LAYOUT", "split")
+    test_fill_matches_oracle(name, dims, ng, ns, nh)
+
+
 def test_fill_cube_sums_deterministic():
     g = np.random.default_rng(3)
     off = _random_plan(g, 5, 4, 2, 3000)
@@ -330,9 +345,9 @@ def test_iteration_shards_merge_to_whole(world):
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_record_chunk_shards_merge_to_whole(monkeypatch, world):
-    # records layout forced with small chunks: each rank's chunk loop covers
-    # only its shard's tiles (vpb_set_shard sizes it), and the shards still
-    # sum to the whole fill
+    # records layout forced with small chunks: each rank fills its hypercube-
+    # aligned shard (its chunks past the shard end are empty launches), and
+    # the shards still sum to the whole fill
     monkeypatch.setenv("VPB_FILL_LAYOUT", "records")
     monkeypatch.setenv("VPB_REC_CHUNK", "8192")
     cfg = P.IntegratorConfig(n_eval=200_000, max_it=3, n_intervals=64, seed=5, batch_size=4096)
@@ -347,7 +362,7 @@ def test_record_chunk_shards_merge_to_whole(monkeypatch, world):
 
     whole, lw = run(1, 0)
     parts = [run(world, r) for r in range(world)]
-    assert lw["chunks"] > 1 and all(p[1]["chunks"] < lw["chunks"] for p in parts)
+    assert lw["chunks"] > 1 and all(p[1]["chunks"] == lw["chunks"] for p in parts)
     acc = [p[0] for p in parts]
     np.testing.assert_array_equal(sum(p[1] for p in acc), whole[1])
     np.testing.assert_array_equal(sum(p[4] for p in acc), whole[4])
