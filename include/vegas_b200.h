@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define VPB_ABI_VERSION 1
+#define VPB_ABI_VERSION 2
 
 /* status codes */
 #define VPB_OK 0
@@ -91,7 +91,16 @@ typedef struct vpb_desc {
   int32_t device;             /* CUDA ordinal; -1 = current device         */
   int32_t max_it;             /* capacity of the per-iteration history     */
   void *stream;               /* cudaStream_t to run on; NULL = own stream */
+  int32_t flags;              /* VPB_FLAG_*                                */
 } vpb_desc;
+
+/* Deterministic mode: bitwise-repeatable map weights (the reference's
+ * repeat criterion, tests/test_acceptance.py:153-190).  The fill runs twice
+ * per iteration with the generic kernel: pass 1's f64 interval sums pick a
+ * per-interval scale 2^k, pass 2 sums round(w2 2^k) with 64-bit integer
+ * atomics -- exact, so neither the update order nor the sharding changes a
+ * bit (the int64 sums are all-reduced exactly).  About 2-3x the fill time. */
+#define VPB_FLAG_DETERMINISTIC 1
 
 /* ---- library ------------------------------------------------------------ */
 int vpb_abi_version(void);

@@ -26,7 +26,8 @@ VPB_ERR_NONFINITE = 3
 VPB_ERR_ASSERT = 4
 VPB_ERR_NCCL = 5
 VPB_ERR_UNSUPPORTED = 6
-ABI_VERSION = 1
+ABI_VERSION = 2
+VPB_FLAG_DETERMINISTIC = 1
 MAX_PARAMS = 64
 MAX_DIMS = 64
 
@@ -48,6 +49,7 @@ class VpbDesc(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("max_it", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("flags", ctypes.c_int32),
     ]
 
 

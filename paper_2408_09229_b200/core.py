@@ -216,7 +216,7 @@ class Integrator:
 
     def __init__(self, f, bounds, config: IntegratorConfig, *, device: int | None = None,
                  distributed: bool | None = None, stream: int | None = None,
-                 exchange: str | None = None):
+                 exchange: str | None = None, deterministic: bool | None = None):
         self.config = config
         self.bounds = [(float(lo), float(hi)) for lo, hi in bounds]
         self.dims = len(self.bounds)
@@ -245,6 +245,10 @@ class Integrator:
         desc.device = _default_device() if device is None else int(device)
         desc.max_it = int(config.max_it)
         desc.stream = stream
+        if deterministic is None:
+            deterministic = os.environ.get("VPB_DETERMINISTIC", "0") == "1"
+        desc.flags = N.VPB_FLAG_DETERMINISTIC if deterministic else 0
+        self.deterministic = bool(deterministic)
         self._lib = lib
         ctx = ctypes.c_void_p()
         N.check(lib.vpb_create(ctypes.byref(desc), ctypes.byref(ctx)), "vpb_create")
@@ -440,7 +444,7 @@ class Integrator:
 def integrate(f, bounds, config: IntegratorConfig | None = None, *,
               batched: bool = False, device: int | None = None,
               distributed: bool | None = None, exchange: str | None = None,
-              **overrides) -> IntegralOutcome:
+              deterministic: bool | None = None, **overrides) -> IntegralOutcome:
     """Integrate a registered device integrand over the box given by bounds.
 
     Same contract as vp/core.py:168-238.  ``f`` is a registered integrand
@@ -455,7 +459,7 @@ def integrate(f, bounds, config: IntegratorConfig | None = None, *,
     timing = PhaseTimes()
     t0 = time.perf_counter()
     integ = Integrator(f, bounds, config, device=device, distributed=distributed,
-                       exchange=exchange)
+                       exchange=exchange, deterministic=deterministic)
     timing.init = time.perf_counter() - t0
     try:
         integ.iterate(config.max_it)

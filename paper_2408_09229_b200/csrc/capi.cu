@@ -284,6 +284,12 @@ struct vpb_ctx {
   long long *ctl = nullptr;     // exchange control word [nonfinite, assert, -first failing run]
   double *hx_f = nullptr;       // pinned host staging (host exchange)
   long long *hx_i = nullptr;
+  long long *hx_q = nullptr;
+  // deterministic mode (VPB_FLAG_DETERMINISTIC): two fill passes, the second
+  // in per-interval fixed point (update.cuh det_*)
+  bool det = false;
+  int *bin_k = nullptr;         // [d*ng] scale exponents from pass 1
+  long long *map_q = nullptr;   // [d*ng] pass-2 fixed-point sums
   // timing
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
@@ -348,6 +354,8 @@ FillArgs fill_args(vpb_ctx *c) {
   a.rec_ch = c->rec_ch;
   a.dig_bits = 0;
   while ((1ll << a.dig_bits) < c->ns) a.dig_bits++;
+  a.det = 0;
+  a.bin_k = c->bin_k;
   a.status = c->status;
   a.err_run = c->err_run;
   a.P = c->P;
@@ -363,6 +371,7 @@ cudaError_t rec_event(vpb_ctx *c, cudaEvent_t e) {
 // A compile-time (integrand, dims) kernel exists and applies: the 3-peak
 // streamed sum of the multipeak kernels needs the registry's 3 peaks.
 bool specialisable(const vpb_ctx *c) {
+  if (c->det) return false;   // deterministic mode runs the generic kernel
   if (!fill_is_specialised(c->id, c->dims)) return false;
   if (c->id == VPB_MULTIPEAK && c->P.p[0] != 3.0) return false;
   return true;
@@ -402,6 +411,30 @@ int join_side(vpb_ctx *c) {
   return VPB_OK;
 }
 
+// Deterministic mode, pass 1: the interval maxima (f64 MAX, exact) and
+// counts (i64 SUM) over all ranks, so every rank derives the same scales.
+int exchange_det_pass1(vpb_ctx *c) {
+  const size_t m = (size_t)c->dims * c->ng;
+  if (c->comm) {
+    NK(ncclGroupStart());
+    NK(ncclAllReduce(c->map_w, c->map_w, m, ncclFloat64, ncclMax, c->comm, c->st));
+    NK(ncclAllReduce(c->map_counts, c->map_counts, m, ncclInt64, ncclSum, c->comm, c->st));
+    NK(ncclGroupEnd());
+    return VPB_OK;
+  }
+  CK(cudaMemcpyAsync(c->hx_f, c->map_w, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(c->hx_i, c->map_counts, sizeof(long long) * m, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->exch_fn(c->exch_user, c->hx_f, (int64_t)m, VPB_DT_F64, VPB_OP_MAX) != 0 ||
+      c->exch_fn(c->exch_user, c->hx_i, (int64_t)m, VPB_DT_I64, VPB_OP_SUM) != 0)
+    return fail(VPB_ERR_NCCL, "host exchange callback failed");
+  CK(cudaMemcpyAsync(c->map_w, c->hx_f, sizeof(double) * m, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->map_counts, c->hx_i, sizeof(long long) * m, cudaMemcpyHostToDevice,
+                     c->st));
+  return VPB_OK;
+}
+
 // The exchange through a host all-reduce callback (vpb_attach_exchange):
 // the same three reductions as the NCCL group, staged through pinned host
 // buffers, synchronously (not graph-capturable).
@@ -412,11 +445,16 @@ int host_exchange(vpb_ctx *c) {
   CK(cudaMemcpyAsync(c->hx_i, c->map_counts, sizeof(long long) * m, cudaMemcpyDeviceToHost,
                      c->st));
   CK(cudaMemcpyAsync(c->hx_i + m, c->ctl, sizeof(long long) * 3, cudaMemcpyDeviceToHost, c->st));
+  if (c->det)
+    CK(cudaMemcpyAsync(c->hx_q, c->map_q, sizeof(long long) * m, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (c->exch_fn(c->exch_user, c->hx_f, (int64_t)nf, VPB_DT_F64, VPB_OP_SUM) != 0 ||
       c->exch_fn(c->exch_user, c->hx_i, (int64_t)m, VPB_DT_I64, VPB_OP_SUM) != 0 ||
-      c->exch_fn(c->exch_user, c->hx_i + m, 3, VPB_DT_I64, VPB_OP_MAX) != 0)
+      c->exch_fn(c->exch_user, c->hx_i + m, 3, VPB_DT_I64, VPB_OP_MAX) != 0 ||
+      (c->det && c->exch_fn(c->exch_user, c->hx_q, (int64_t)m, VPB_DT_I64, VPB_OP_SUM) != 0))
     return fail(VPB_ERR_NCCL, "host exchange callback failed");
+  if (c->det)
+    CK(cudaMemcpyAsync(c->map_q, c->hx_q, sizeof(long long) * m, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->accf, c->hx_f, sizeof(double) * nf, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemcpyAsync(c->map_counts, c->hx_i, sizeof(long long) * m, cudaMemcpyHostToDevice,
                      c->st));
@@ -438,8 +476,34 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
     CK(cudaMemsetAsync(c->hc_glob, 0, sizeof(unsigned long long) * m, c->st));
   }
   FillArgs a = fill_args(c);
+  const bool exch = c->comm || c->exch_fn;
+  const unsigned mb = (unsigned)((m + 255) / 256);
   if (timed) CK(cudaEventRecord(c->f0, c->st));
   if (k0) CK(rec_event(c, k0));
+  if (c->det) {
+    // deterministic mode, pass 1: per interval the largest w2 and the count
+    // (both exact) pick each interval's fixed-point scale for pass 2
+    a.det = 1;
+    CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, a));
+    if (c->smem_hist) {
+      hist_reduce_max_kernel<<<mb, 256, 0, c->st>>>(
+          reinterpret_cast<const unsigned long long *>(c->hw_part), c->hc_part, c->grid_tiles,
+          (long long)m, c->map_w, c->map_counts, c->status);
+    } else {
+      CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice,
+                         c->st));
+      hist_glob_convert_kernel<<<mb, 256, 0, c->st>>>(c->hc_glob, (long long)m, c->map_counts);
+    }
+    CK(cudaGetLastError());
+    if (exch) TRY(exchange_det_pass1(c));   // the same scales on every rank
+    det_scale_kernel<<<mb, 256, 0, c->st>>>(c->map_w, c->map_counts, (long long)m, c->bin_k,
+                                            c->status);
+    if (!c->smem_hist) {
+      CK(cudaMemsetAsync(c->hw_glob, 0, sizeof(double) * m, c->st));
+      CK(cudaMemsetAsync(c->hc_glob, 0, sizeof(unsigned long long) * m, c->st));
+    }
+    a.det = 2;
+  }
   if (c->split) {
     CK(launch_fill_split(c->id, c->dims, c->grid, c->smem, c->st, a));
   } else if (!c->records) {
@@ -479,7 +543,24 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   TRY(fork_side(c));   // histogram reduction (side) || cube-chain fixup (st)
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
   cudaStream_t hs_st = c->side;
-  if (c->records) {
+  if (c->det) {   // pass 2's exact fixed-point sums -> map_q (-> map_w after any exchange)
+    if (c->smem_hist)
+      hist_reduce_q_kernel<<<mb, 256, 0, hs_st>>>(
+          reinterpret_cast<const unsigned long long *>(c->hw_part), c->grid_tiles, (long long)m,
+          c->map_q, c->status);
+    else
+      CK(cudaMemcpyAsync(c->map_q, c->hw_glob, sizeof(long long) * m, cudaMemcpyDeviceToDevice,
+                         hs_st));
+    if (!c->smem_hist)
+      hist_glob_convert_kernel<<<mb, 256, 0, hs_st>>>(c->hc_glob, (long long)m, c->map_counts);
+    else
+      hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, hs_st>>>(
+          c->hw_part, c->hc_part, c->grid_tiles, (long long)m, c->map_w, c->map_counts,
+          c->status);   // counts (the f64 part of the slices is the fixed point: map_w redone below)
+    if (!exch)
+      det_convert_kernel<<<mb, 256, 0, hs_st>>>(c->map_q, c->bin_k, (long long)m, c->map_w,
+                                                c->status);
+  } else if (c->records) {
     const size_t m0 = (size_t)c->rec_k0 * c->ng;   // rows histogrammed by the fill itself
     if (m0 > 0)
       hist_reduce_kernel<<<(unsigned)((m0 + 31) / 32), dim3(32, 8), 0, hs_st>>>(
@@ -498,7 +579,6 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
                                                                            c->map_counts);
   }
   CK(cudaGetLastError());
-  const bool exch = c->comm || c->exch_fn;
   if (!defer_join || exch) TRY(join_side(c));
   if (exch) {
     // one exchange per iteration: map_w|s1|s2 (f64 sum), map_counts (i64
@@ -511,11 +591,16 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
                        c->comm, c->st));
       NK(ncclAllReduce(c->map_counts, c->map_counts, m, ncclInt64, ncclSum, c->comm, c->st));
       NK(ncclAllReduce(c->ctl, c->ctl, 3, ncclInt64, ncclMax, c->comm, c->st));
+      if (c->det)   // exact: the fixed-point sums do not depend on the sharding
+        NK(ncclAllReduce(c->map_q, c->map_q, m, ncclInt64, ncclSum, c->comm, c->st));
       NK(ncclGroupEnd());
     } else {
       TRY(host_exchange(c));
     }
     ctl_unpack_kernel<<<1, 1, 0, c->st>>>(c->status, c->err_run, c->ctl);
+    if (c->det)
+      det_convert_kernel<<<mb, 256, 0, c->st>>>(c->map_q, c->bin_k, (long long)m, c->map_w,
+                                                c->status);
     CK(cudaGetLastError());
   }
   return VPB_OK;
@@ -655,7 +740,7 @@ void free_ctx(vpb_ctx *c) {
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec,
-                  c->ctl};
+                  c->ctl, c->bin_k, c->map_q};
   for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
@@ -673,6 +758,7 @@ void free_ctx(vpb_ctx *c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->hx_f) cudaFreeHost(c->hx_f);
   if (c->hx_i) cudaFreeHost(c->hx_i);
+  if (c->hx_q) cudaFreeHost(c->hx_q);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
 }
 
@@ -740,6 +826,8 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   c->id = d->integrand;
   c->max_it = d->max_it;
   if (const char *g = std::getenv("VPB_NO_GRAPH")) c->use_graph = !(g[0] == '1');
+  c->det = (d->flags & VPB_FLAG_DETERMINISTIC) != 0;
+  if (const char *e = std::getenv("VPB_DETERMINISTIC")) c->det = c->det || e[0] == '1';
   c->P.n = d->n_params;
   for (int i = 0; i < d->n_params; i++) c->P.p[i] = d->params[i];
   c->bounds.assign(d->bounds, d->bounds + 2 * d->dims);
@@ -808,6 +896,10 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     return bail(fail(VPB_ERR_CUDA, "refine smem attribute"));
   A(c->explicit_rb, 1);
   A(c->ctl, 3);
+  if (c->det) {
+    A(c->bin_k, m);
+    A(c->map_q, m);
+  }
   // fill geometry: shared histograms when they fit next to the edges
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
@@ -831,7 +923,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // VPB_HIST_COPIES=2: two copies of the shared f64 sums (one per half-warp)
   // when they fit -- fewer same-interval collisions inside a CAS instruction
   // (measured: cfg4a/b -1.0%, cfg2 -0.7% fill time, cfg1/cfg3 neutral)
-  int want_copies = 2;
+  int want_copies = c->det ? 1 : 2;
   if (const char *e = std::getenv("VPB_HIST_COPIES")) want_copies = std::atoi(e) == 2 ? 2 : 1;
   for (int cp = want_copies; cp >= 1 && c->smem_hist && !fits; cp--)
     for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
@@ -869,7 +961,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   }
   if (c->smem > (size_t)optin)
     return bail(fail(VPB_ERR_UNSUPPORTED, "map edges do not fit in shared memory"));
-  c->records = !c->smem_hist && forced != "global" && c->ng <= 65535 &&
+  c->records = !c->smem_hist && forced != "global" && !c->det && c->ng <= 65535 &&
                hist_records_smem(c->ng) <= (size_t)optin;
   const bool spec = specialisable(c);
   const int layout = c->split                 ? LAYOUT_SPLIT
@@ -1026,6 +1118,7 @@ int vpb_attach_exchange(vpb_ctx *c, int32_t world, int32_t rank, vpb_allreduce_f
   if (!c->hx_f) {
     CK(cudaMallocHost(&c->hx_f, sizeof(double) * (m + 2 * (size_t)c->n_cubes)));
     CK(cudaMallocHost(&c->hx_i, sizeof(long long) * (m + 3)));
+    if (c->det) CK(cudaMallocHost(&c->hx_q, sizeof(long long) * m));
   }
   // host callbacks cannot live in a captured graph: iterations are enqueued
   // directly, synchronising at the exchange

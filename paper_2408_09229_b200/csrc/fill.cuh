@@ -40,9 +40,6 @@ namespace vpb {
 #ifndef VPB_FILL_NT
 #define VPB_FILL_NT 640
 #endif
-#ifndef VPB_HIST_MATCH
-#define VPB_HIST_MATCH 0
-#endif
 #ifndef VPB_FILL_RPT
 #define VPB_FILL_RPT 16   // measured: 8 and 32 lose on cfg1/cfg2 (32: cfg4 -1%, cfg1 +69%)
 #endif
@@ -107,6 +104,8 @@ struct FillArgs {
   long long rec_ch;             // records per chunk (a multiple of FILL_TILE)
   int pairs;                    // 1: (E[i], dx[i]) pair table instead of the edge rows
   int hs;                       // row stride of the shared histograms [interval][axis]
+  int det;                      // deterministic mode pass (generic kernel): 0/1 f64, 2 fixed point
+  const int *bin_k;             // det pass 2: per (axis, interval) scale exponent [d][ng]
   int *status;                  // bit0 non-finite, bit1 assert
   unsigned long long *err_run;  // min run index with a non-finite value
   IParams P;
@@ -687,6 +686,38 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
               atomicAdd(&s_hwl[idx[jl]], w2);
               atomicAdd(&s_hc[idx[jl]], 1u);
             }
+          } else if (RT && a.det == 1) {
+            // deterministic mode, pass 1: per (axis, interval) the largest w2
+            // (u64 max of the non-negative doubles' bit patterns: exact and
+            // order-independent) and the count pick pass 2's scale
+            for (int j = 0; j < d; j++) {
+              const int b = iv[j];
+              const unsigned long long wb = (unsigned long long)__double_as_longlong(w2);
+              if (a.smem_hist) {
+                atomicMax(reinterpret_cast<unsigned long long *>(s_hw) + (size_t)b * hs + j, wb);
+                atomicAdd(&s_hc[b * hs + j], 1u);
+              } else {
+                atomicMax(reinterpret_cast<unsigned long long *>(a.hw_glob) + (size_t)j * ng + b, wb);
+                atomicAdd(&a.hc_glob[j * ng + b], 1ull);
+              }
+            }
+          } else if (RT && a.det == 2) {
+            // deterministic mode, pass 2: each w2 in the fixed point of its
+            // (axis, interval)'s scale 2^k (count x max < 2^62), summed with
+            // 64-bit integer atomics -- exact, so the update order cannot
+            // change the bits (vpb_desc flags)
+            for (int j = 0; j < d; j++) {
+              const int b = iv[j];
+              const int kb = __ldg(a.bin_k + (size_t)j * ng + b);
+              const unsigned long long q = __double2ull_rn(scalbn(w2, kb));
+              if (a.smem_hist) {
+                atomicAdd(reinterpret_cast<unsigned long long *>(s_hw) + (size_t)b * hs + j, q);
+                atomicAdd(&s_hc[b * hs + j], 1u);
+              } else {
+                atomicAdd(reinterpret_cast<unsigned long long *>(a.hw_glob) + (size_t)j * ng + b, q);
+                atomicAdd(&a.hc_glob[j * ng + b], 1ull);
+              }
+            }
           } else if (!RT || a.smem_hist) {
             // Lane-rotated dimension order: at step s lane l updates dim
             // (s + l) mod d.  Lanes of a warp usually sit in the same cube,
@@ -727,32 +758,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
             double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
 #pragma unroll
             for (int j = 0; j < (D > 0 ? D : d); j++) {
-#if VPB_HIST_MATCH
-              // lanes of this warp hitting the same interval: the lowest one
-              // adds the group's w2 (summed in lane order) and count, so the
-              // CAS loop never retries on an intra-warp collision
-              const unsigned act = __activemask();
-              const unsigned grp = __match_any_sync(act, idx[j]);
-              if (grp == (1u << lane)) {
-                atomicAdd(&s_hwl[idx[j]], w2);
-                atomicAdd(&s_hc[idx[j]], 1u);
-              } else {
-                double gs = 0.0;
-                unsigned mm = grp;
-                while (mm) {
-                  const int src = __ffs(mm) - 1;
-                  mm &= mm - 1;
-                  gs = __dadd_rn(gs, __shfl_sync(grp, w2, src));
-                }
-                if (lane == __ffs(grp) - 1) {
-                  atomicAdd(&s_hwl[idx[j]], gs);
-                  atomicAdd(&s_hc[idx[j]], (unsigned)__popc(grp));
-                }
-              }
-#else
               atomicAdd(&s_hwl[idx[j]], w2);
               atomicAdd(&s_hc[idx[j]], 1u);
-#endif
             }
             }
           } else {

@@ -59,6 +59,7 @@ int fill_is_specialised(int id, int dims) {
 
 cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
                         const FillArgs &a) {
+  if (a.det) return launch_fill_generic(id, grid, smem, st, a);   // deterministic mode
 #define X(I, D)                                                                  \
   if (id == I && dims == D) {                                                    \
     if (a.records) return launch_one<I, D, LAYOUT_RECORDS>(grid, smem, st, a);   \

@@ -568,6 +568,56 @@ __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_par
   }
 }
 
+// ---- deterministic mode (vpb_desc flags: VPB_FLAG_DETERMINISTIC) --------
+// Pass 1 finds, per (axis, interval), the largest w2 (u64 max of the bit
+// patterns, exact) and the count n; k = 61 - ilogb(max) - ceil(log2 n) keeps
+// the pass-2 fixed-point sum below 2^62.  Pass 2 adds round(w2 * 2^k) with
+// 64-bit integer atomics -- exact, hence independent of the update order and
+// of the sharding (the int64 sums are all-reduced exactly) -- and map_w =
+// sum * 2^-k rounds once.  Every input of k is exact, so the scales, and with
+// them the sums, repeat bitwise.  Rounding: <= n/2 units of 2^-62 n max, i.e.
+// ~1e-16 relative for any interval whose values are within 1e3 of each other
+// (the reference's own sequential f64 sums carry the same order of error).
+__global__ void hist_reduce_max_kernel(const unsigned long long *hw_part, const unsigned *hc_part,
+                                       int nparts, long long m, double *map_w,
+                                       long long *map_counts, const int *status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || *status) return;
+  unsigned long long mx = 0;
+  long long c = 0;
+  for (int b = 0; b < nparts; b++) {
+    mx = max(mx, hw_part[(size_t)b * m + i]);
+    c += hc_part[(size_t)b * m + i];
+  }
+  map_w[i] = __longlong_as_double((long long)mx);
+  map_counts[i] = c;
+}
+__global__ void det_scale_kernel(const double *map_max, const long long *map_counts, long long m,
+                                 int *bin_k, const int *status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || *status) return;
+  const double v = map_max[i];
+  const long long n = map_counts[i];
+  int lg = 0;
+  while ((1ll << lg) < n) lg++;   // ceil(log2 n)
+  bin_k[i] = (v > 0.0 && isfinite(v)) ? 61 - ilogb(v) - lg : 0;
+}
+// fixed-point slices (u64 bit patterns in the f64 slice buffers) -> map_q
+__global__ void hist_reduce_q_kernel(const unsigned long long *hw_part, int nparts, long long m,
+                                     long long *map_q, const int *status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || *status) return;
+  unsigned long long t = 0;
+  for (int b = 0; b < nparts; b++) t += hw_part[(size_t)b * m + i];
+  map_q[i] = (long long)t;
+}
+__global__ void det_convert_kernel(const long long *map_q, const int *bin_k, long long m,
+                                   double *map_w, const int *status) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m || *status) return;
+  map_w[i] = scalbn(__ull2double_rn((unsigned long long)map_q[i]), -bin_k[i]);
+}
+
 // The exchange's control word, all-reduced with MAX next to the accumulators
 // so that every rank sees every rank's failure (vp/executor.py:151-165: the
 // reference re-raises the lowest failing worker's exception for the whole

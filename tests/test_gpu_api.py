@@ -156,6 +156,52 @@ def test_determinism():
         assert o.mean == pytest.approx(outs[0].mean, rel=1e-12)
 
 
+def test_deterministic_mode_bitwise_repeats():
+    # pkg/tests/test_acceptance.py:153-190 at full strength: integrate() repeats
+    # bit for bit (mean, sigma, chi2, every iteration) with the deterministic
+    # fill (two passes, per-interval fixed point summed with integer atomics)
+    def run(**kw):
+        return integrate("gaussian", [(0, 1)] * 4, n_eval=50_000, max_it=8, skip=2, seed=17,
+                         batch_size=4096, **kw)
+    outs = [run(deterministic=True) for _ in range(3)]
+    for o in outs[1:]:
+        assert (o.mean, o.sigma, o.chi2_dof) == (outs[0].mean, outs[0].sigma, outs[0].chi2_dof)
+        assert [(r.estimate, r.variance) for r in o.iterations] == \
+            [(r.estimate, r.variance) for r in outs[0].iterations]
+        assert o.evals_per_iteration == outs[0].evals_per_iteration
+    fast = run()
+    assert fast.evals_per_iteration == outs[0].evals_per_iteration
+    np.testing.assert_allclose([r.estimate for r in fast.iterations],
+                               [r.estimate for r in outs[0].iterations], rtol=1e-11)
+
+
+@pytest.mark.parametrize("name,dims,n_eval,ng,its", [
+    ("gaussian", 4, 1_000_000, 1000, 5),        # cfg1 geometry: shared-memory fixed point
+    ("multipeak8", 8, 2_000_000, 1024, 4),
+    ("gaussian20", 20, 3_000_000, 1024, 3),     # d*ng too large: global 64-bit atomics
+])
+def test_deterministic_mode_matches_oracle(name, dims, n_eval, ng, its):
+    import oracle as O
+    bounds = [(0.0, 1.0)] * dims
+    res = []
+    for _ in range(2):
+        with P.Integrator(name, bounds, P.IntegratorConfig(n_eval=n_eval, max_it=its,
+                                                           n_intervals=ng, seed=3),
+                          deterministic=True) as it:
+            it.iterate(its)
+            est, var, ev = it.history()
+            res.append((est, var, ev, it.edges()))
+    for a, b in zip(res[0], res[1]):
+        np.testing.assert_array_equal(a, b)       # bitwise repeat, edges included
+    ref = O.integrate(name, bounds, n_eval, max_it=its, n_intervals=ng, seed=3,
+                      workers=os.cpu_count() or 1)
+    est, var, ev, edges = res[0]
+    np.testing.assert_array_equal(ev, ref.evals)
+    np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
+    np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
+    np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=0)
+
+
 def test_fill_counts_deterministic_and_shard_invariant():
     from paper_2408_09229_b200 import ops
     from paper_2408_09229_b200.distributed import partition_runs

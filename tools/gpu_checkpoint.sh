@@ -13,8 +13,9 @@ for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5 ra10; do
 done
 # instruction counts into profiles/fill_traffic.json before the bench lines
 # read them (roofline.issue)
-python tools/refresh_profiles.py gpurun_out/$TAG round1 > /dev/null
-timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/$TAG/tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/$TAG/tests.log
+python tools/refresh_profiles.py gpurun_out/$TAG ${ROUND:-round2} > /dev/null
+timeout 300 python tools/fp64_peak.py gpurun_out/$TAG/fp64_peak.json > /dev/null 2>&1; echo "fp64 peak rc=$?"
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/$TAG/tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/$TAG/tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/$TAG/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 600 python bench.py > gpurun_out/$TAG/bench_default.json 2> gpurun_out/$TAG/bench_default.err; echo "bench rc=$?"; cat gpurun_out/$TAG/bench_default.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/$TAG/bench_ref.json 2>&1; echo "ref rc=$?"
@@ -22,5 +23,8 @@ for c in cfg1 cfg3 cfg4a cfg4b cfg5 ra10; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/$TAG/bench_$c.json 2> gpurun_out/$TAG/bench_$c.err; echo "bench $c rc=$?"
 done
 bash tools/gpu_profile.sh cfg2 $TAG/p
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/$TAG/p_launches_cfg1.csv python bench.py --config cfg1 --steps 3 --warmup 3 --no-cpu \
+  > /dev/null 2>&1; echo "cfg1 launches rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 2 -c 1 \
   -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 4 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"

@@ -35,9 +35,23 @@ for f in sorted(os.listdir(src)):
         if d is not None:
             name = "bench_cfg2.json" if f == "bench_default.json" else f
             json.dump(d, open(os.path.join(dst, name), "w"), indent=1)
-for f in ("p_launches_cfg2.csv",):
+for f, g in (("p_launches_cfg2.csv", "launches_cfg2.csv"), ("p_launches_cfg1.csv", "launches_cfg1.csv"),
+             ("fp64_peak.json", "fp64_peak.json"), ("bench_ref.json", "bench_ref.json"),
+             ("tests.log", "gpu_tests.log")):
     if os.path.exists(os.path.join(src, f)):
-        shutil.copy(os.path.join(src, f), os.path.join(dst, "launches_cfg2.csv"))
+        shutil.copy(os.path.join(src, f), os.path.join(dst, g))
+for c in ("cfg1", "cfg2"):
+    lp = os.path.join(dst, "launches_%s.csv" % c)
+    if os.path.exists(lp):
+        tab = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_table.py"), lp],
+                             capture_output=True, text=True).stdout
+        open(os.path.join(dst, "launches_%s_table.txt" % c), "w").write(tab)
+rep4 = os.path.join(src, "p_fill_cfg4b.ncu-rep")
+if os.path.exists(rep4) and os.path.exists(os.path.join(src, "bench_cfg4b.json")):
+    ev4 = json_line(os.path.join(src, "bench_cfg4b.json"))["config"]["evals_per_step"]
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep4,
+                          str(ev4)], capture_output=True, text=True).stdout
+    open(os.path.join(dst, "fill_cfg4b_ncu_summary.json"), "w").write(out)
 rep = os.path.join(src, "p_fill_cfg2.ncu-rep")
 if os.path.exists(rep):
     evals = json_line(os.path.join(src, "bench_default.json"))["config"]["evals_per_step"]
