@@ -319,6 +319,8 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
     e_integ.close()
 
     layout = integ.fill_layout()
+    fx = integ.fx_stats()
+    fx["mode"] = "fixed point (per-interval predicted scale)" if fx["enabled"] else "f64 CAS"
     if rank == 0:
         ops = fp64_ops_per_eval(cfg)
         # fill kernel: per-rank evaluations = its shard of each plan
@@ -385,6 +387,9 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
             "gpu_launches": layout["launches_per_iteration"] * steps,
             "clocks": clk,
             "estimates": {"last": float(est[-1]), "sigma_last": float(np.sqrt(var[-1]))},
+            # fixed-point interval histograms (fill.cuh LAYOUT_FX): iterations
+            # filled in fixed point, redone in f64, values spilled to f64
+            "histograms": fx,
         }
         print(json.dumps(line), flush=True)
     integ.close()

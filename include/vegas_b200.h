@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define VPB_ABI_VERSION 2
+#define VPB_ABI_VERSION 3
 
 /* status codes */
 #define VPB_OK 0
@@ -173,6 +173,13 @@ int vpb_timing(vpb_ctx *ctx, int32_t first, int32_t count, double *iter_ms,
  * the number of this library's kernel launches per iteration. */
 int vpb_fill_layout(vpb_ctx *ctx, int32_t *layout, int32_t *n_chunks,
                     int32_t *launches_per_iteration);
+/* Fixed-point interval histograms (FX mode; no reference counterpart -- an
+ * implementation choice behind vp/kernels.py:100-105's MapWeights sums):
+ * out = [enabled for this context, iterations filled in fixed point,
+ * iterations whose fixed-point sums failed the precision / wrap-around proof
+ * and were refilled in f64, values summed in f64 because they exceeded the
+ * fixed-point range].  Synchronises the context's stream. */
+int vpb_fx_stats(vpb_ctx *ctx, int64_t out[4]);
 /* Measured FP64 pipe throughput (DFMA chains on every SM; one FMA = 1 op):
  * the roofline denominator for the FP64-issue-bound fill. */
 int vpb_fp64_peak(int32_t device, double *ops_per_s);

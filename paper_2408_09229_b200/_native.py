@@ -26,7 +26,7 @@ VPB_ERR_NONFINITE = 3
 VPB_ERR_ASSERT = 4
 VPB_ERR_NCCL = 5
 VPB_ERR_UNSUPPORTED = 6
-ABI_VERSION = 2
+ABI_VERSION = 3
 VPB_FLAG_DETERMINISTIC = 1
 MAX_PARAMS = 64
 MAX_DIMS = 64
@@ -85,6 +85,7 @@ SIGNATURES = {
     "vpb_timing": [_P, _I32, _I32, _c.POINTER(_F64), _c.POINTER(_F64)],
     "vpb_fp64_peak": [_I32, _c.POINTER(_F64)],
     "vpb_fill_layout": [_P, _c.POINTER(_I32), _c.POINTER(_I32), _c.POINTER(_I32)],
+    "vpb_fx_stats": [_P, _P],
     "vpb_set_edges": [_P, _P],
     "vpb_get_edges": [_P, _P],
     "vpb_set_allocation": [_P, _P],

@@ -348,6 +348,15 @@ class Integrator:
         return {"layout": self._LAYOUTS.get(lay.value, str(lay.value)), "chunks": ch.value,
                 "launches_per_iteration": ln.value}
 
+    def fx_stats(self) -> dict:
+        """Fixed-point interval histograms (vpb_fx_stats): whether the mode is
+        on for this context, iterations filled in fixed point, iterations
+        refilled in f64 after a failed proof, values summed in f64 instead."""
+        out = np.zeros(4, dtype=np.int64)
+        N.check(self._lib.vpb_fx_stats(self._ctx, N.ptr(out)))
+        return {"enabled": bool(out[0]), "fixed_iterations": int(out[1]),
+                "refilled": int(out[2]), "spilled_values": int(out[3])}
+
     def last_fill_ms(self) -> float:
         t = ctypes.c_double()
         N.check(self._lib.vpb_last_fill_ms(self._ctx, ctypes.byref(t)))

@@ -290,6 +290,13 @@ struct vpb_ctx {
   bool det = false;
   int *bin_k = nullptr;         // [d*ng] scale exponents from pass 1
   long long *map_q = nullptr;   // [d*ng] pass-2 fixed-point sums
+  // FX mode (fill.cuh LAYOUT_FX): fixed-point interval histograms with
+  // predicted scales, proven by fx_reduce_kernel or redone in f64
+  bool fx = false;
+  int fx_L = 52;                // values below 2^L units are summed in fixed point
+  FxState *fxs = nullptr;
+  int *fx_k = nullptr, *fx_kmin = nullptr;
+  double *fx_spill = nullptr;
   // timing
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
@@ -359,6 +366,13 @@ FillArgs fill_args(vpb_ctx *c) {
   a.status = c->status;
   a.err_run = c->err_run;
   a.P = c->P;
+  a.gate = nullptr;
+  a.fx = 0;
+  a.fx_k = c->fx_k;
+  a.fx_kmin = c->fx_kmin;
+  a.fx_spill = c->fx_spill;
+  a.fx_lim = 0x43300000u + (1u << (c->fx_L - 32));
+  a.fx_nspill = c->fxs ? &c->fxs->spills : nullptr;
   return a;
 }
 
@@ -504,6 +518,21 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
     }
     a.det = 2;
   }
+  if (c->fx) {
+    // fixed-point fill (runs when fx_begin_kernel opens it), the proof and
+    // reduction of its sums; the f64 fill below runs only if either says so
+    fx_begin_kernel<<<1, 1, 0, c->st>>>(c->fxs, c->sched, c->dims, c->status);
+    FillArgs ax = a;
+    ax.gate = &c->fxs->gate_fx;
+    ax.fx = 1;
+    CK(launch_fill(c->id, c->dims, c->grid, c->smem, c->st, ax));
+    fx_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, c->st>>>(
+        reinterpret_cast<const unsigned long long *>(c->hw_part), c->hc_part, c->grid_tiles,
+        (long long)m, c->ng, c->dims, c->fx_k, c->fx_kmin, c->fx_L, c->map_w, c->map_counts, c->fx_spill,
+        c->fxs, c->status);
+    CK(cudaGetLastError());
+    a.gate = &c->fxs->gate_f64;
+  }
   if (c->split) {
     CK(launch_fill_split(c->id, c->dims, c->grid, c->smem, c->st, a));
   } else if (!c->records) {
@@ -571,7 +600,7 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   } else if (c->smem_hist) {
     hist_reduce_kernel<<<(unsigned)((m + 31) / 32), dim3(32, 8), 0, hs_st>>>(
         c->hw_part, c->hc_part, c->grid_tiles, (long long)m, c->map_w, c->map_counts,
-        c->status);
+        c->status, c->fx ? &c->fxs->gate_f64 : nullptr);
   } else {
     CK(cudaMemcpyAsync(c->map_w, c->hw_glob, sizeof(double) * m, cudaMemcpyDeviceToDevice, hs_st));
     hist_glob_convert_kernel<<<(unsigned)((m + 255) / 256), 256, 0, hs_st>>>(c->hc_glob,
@@ -613,7 +642,8 @@ int enqueue_update(vpb_ctx *c, int record) {
   // or after the all-reduce) || results + allocation (st)
   if (!c->side_open) TRY(fork_side(c));
   refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->side>>>(
-      c->edges, c->map_w, c->map_counts, c->ng, c->alpha, c->refine_scr, c->status, nullptr);
+      c->edges, c->map_w, c->map_counts, c->ng, c->alpha, c->refine_scr, c->status, nullptr,
+      c->fx ? c->fx_k : nullptr, c->fx_kmin, c->fxs);
   cube_terms_kernel<<<(unsigned)((c->n_cubes + 255) / 256), 256, 0, c->st>>>(
       c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, c->pwterms, c->status);
   results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
@@ -740,7 +770,7 @@ void free_ctx(vpb_ctx *c) {
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec,
-                  c->ctl, c->bin_k, c->map_q};
+                  c->ctl, c->bin_k, c->map_q, c->fxs, c->fx_k, c->fx_kmin, c->fx_spill};
   for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
@@ -923,7 +953,13 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // VPB_HIST_COPIES=2: two copies of the shared f64 sums (one per half-warp)
   // when they fit -- fewer same-interval collisions inside a CAS instruction
   // (measured: cfg4a/b -1.0%, cfg2 -0.7% fill time, cfg1/cfg3 neutral)
-  int want_copies = c->det ? 1 : 2;
+  // The FX fill (fixed-point histograms, below) keeps one copy: its
+  // updates do not collide in CAS loops, and one copy leaves room for the
+  // pair table (cfg2: pairs 128 KB + 64 + 32 KB).
+  bool fx_want = d->n_eval >= 10000000;
+  if (const char *e = std::getenv("VPB_HIST_FIXED")) fx_want = e[0] == '1';
+  fx_want = fx_want && !c->det && specialisable(c);
+  int want_copies = (c->det || fx_want) ? 1 : 2;
   if (const char *e = std::getenv("VPB_HIST_COPIES")) want_copies = std::atoi(e) == 2 ? 2 : 1;
   for (int cp = want_copies; cp >= 1 && c->smem_hist && !fits; cp--)
     for (int pass = 0; pass < 4 && c->smem_hist && !fits; pass++) {
@@ -991,6 +1027,33 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
       return bail(fail(VPB_ERR_CUDA, "fill kernel cannot be resident"));
     c->grid = sms * per_sm;
     c->grid_tiles = c->grid;
+  }
+  // FX mode: compiled (id, dims) kernels with shared histograms (pairs or
+  // edge rows), not in deterministic mode.  Each CTA slice of an interval
+  // must stay below 2^64 units: with values < 2^L and at most ~cpb runs per
+  // (CTA, interval) -- runs are uniform over the intervals, x4 headroom,
+  // checked exactly by fx_reduce_kernel -- L = 62 - ceil(log2 cpb) <= 52 (the
+  // DFMA's mantissa).  The count field is 20 bits next to the scale's
+  // biased exponent; a count past 2^20 changes the exponent bits, which
+  // fx_reduce_kernel checks.
+  // Default on from 1e7 evaluations per iteration (below that the fill is a
+  // small part of the step and the extra launches cost more than they save);
+  // VPB_HIST_FIXED=0|1 forces it off / on where eligible.
+  {
+    const long long cap_runs = c->ntiles_cap * FILL_TILE;
+    const long long cpb = cap_runs / ((long long)c->grid_tiles * c->ng) + 1;
+    int lg = 0;
+    while ((1ll << lg) < cpb) lg++;
+    c->fx_L = std::min(52, 62 - lg);
+    c->fx = fx_want && !c->split && !c->records && c->smem_hist && spec &&
+            (layout == LAYOUT_PAIRS || layout == LAYOUT_EDGES) &&
+            c->fx_L >= VPB_FX_T + 6;
+    if (c->fx) {
+      A(c->fxs, 1);
+      A(c->fx_k, m);
+      A(c->fx_kmin, (size_t)c->dims);
+      A(c->fx_spill, m);
+    }
   }
   if (c->records) {
     c->n_groups = (c->dims - c->rec_k0 + 7) / 8;
@@ -1148,6 +1211,12 @@ int vpb_reset(vpb_ctx *c) {
   unsigned long long big = ~0ull;
   CK(cudaMemcpy(c->err_run, &big, sizeof(big), cudaMemcpyHostToDevice));
   CK(cudaMemset(c->h_evals, 0, sizeof(long long) * c->max_it));
+  if (c->fx) {
+    FxState f{};
+    f.enabled = 1;
+    CK(cudaMemcpy(c->fxs, &f, sizeof(f), cudaMemcpyHostToDevice));
+    CK(cudaMemset(c->fx_spill, 0, sizeof(double) * (size_t)c->dims * c->ng));
+  }
   TRY(uniform_allocation(c));
   CK(cudaStreamSynchronize(c->st));
   c->it_enq = 0;
@@ -1278,7 +1347,23 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   // reduce, cube_terms, results_leaf, results_tree, alloc, refine, end
   const int n_rec = c->dims - c->rec_k0;
   const int fill = c->records ? c->n_chunks * (1 + (n_rec >= 8) + (n_rec % 8 != 0)) : 1;
-  if (launches) *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1;
+  if (launches)
+    *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1 + (c->fx ? 3 : 0);
+  return VPB_OK;
+}
+
+int vpb_fx_stats(vpb_ctx *c, int64_t out[4]) {
+  if (!c || !out) return fail(VPB_ERR_INVALID, "null argument");
+  out[0] = c->fx ? 1 : 0;
+  out[1] = out[2] = out[3] = 0;
+  if (!c->fx) return VPB_OK;
+  TRY(setdev(c));
+  CK(cudaStreamSynchronize(c->st));
+  FxState f{};
+  CK(cudaMemcpy(&f, c->fxs, sizeof(f), cudaMemcpyDeviceToHost));
+  out[1] = f.n_fx;
+  out[2] = f.n_redo;
+  out[3] = (int64_t)f.spills;
   return VPB_OK;
 }
 

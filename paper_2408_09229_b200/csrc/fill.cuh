@@ -109,6 +109,21 @@ struct FillArgs {
   int *status;                  // bit0 non-finite, bit1 assert
   unsigned long long *err_run;  // min run index with a non-finite value
   IParams P;
+  // gate: the launch does nothing unless *gate != 0 (nullptr: always runs).
+  // The fixed-point fill and the f64 fill of an iteration are both in the
+  // captured graph; fx_begin_kernel / fx_reduce_kernel open one of them.
+  const int *gate;
+  // FX layouts (fixed-point interval histograms, see below): per (axis,
+  // interval) predicted scale exponents and their per-axis minima (written
+  // by refine_kernel for the next iteration), the global f64 sums of the
+  // values too large for the fixed point, the hi-word limit of
+  // RN(w2 2^k) + 2^52 below which a value is summed in fixed point
+  const int *fx_k;              // [d][ng]
+  const int *fx_kmin;           // [d]
+  double *fx_spill;             // [d][ng]
+  unsigned fx_lim;               // 0x43300000 + 2^(L-32): hi word of 2^52 + 2^L
+  unsigned long long *fx_nspill;   // count of spilled values (statistics)
+  int fx;                       // launch the FX layout of the compiled kernel
 };
 
 struct SegItem {   // a partial cube segment (key < 0: none)
@@ -166,6 +181,47 @@ constexpr int LAYOUT_RUNTIME = 3;   // generic kernel: a.smem_hist / a.records /
 // commutative IEEE ops, i.e. get bit-identical f, jf and w2; CTA 0 keeps the
 // cube sums.
 constexpr int LAYOUT_SPLIT = 4;
+// FX (bit 3 on EDGES or PAIRS): the interval histograms in per-(axis,
+// interval) fixed point instead of f64 -- two u32 limbs per interval, the
+// interval's scale exponent in the top byte of its u32 count word.  A value
+// w2 becomes q = RN(w2 2^k) by one DFMA against 2^52 and is added with a
+// value-returning u32 atomic on the low limb and a plain one (high bits +
+// carry) on the high limb: three u32 shared atomics that issue back to back
+// for all d axes, instead of d serialised LDS -> DADD -> ATOMS.CAST.SPIN
+// loops (the f64 CAS loop costs ~2x the shared-memory wavefronts and is the
+// L1 bound of the cfg4 fill).  The scales are predicted from the previous
+// iteration's interval averages and the new map (refine_kernel); values at
+// or above 2^L units go to a global f64 sum instead (fx_spill), and
+// fx_reduce_kernel proves every interval's fixed-point sum precise to 2^-P
+// of its total and free of wrap-around, or orders the iteration's fill
+// redone in f64 (the gated second fill in the graph).
+constexpr int LAYOUT_FX = 8;
+constexpr int LAYOUT_EDGES_FX = LAYOUT_EDGES | LAYOUT_FX;
+constexpr int LAYOUT_PAIRS_FX = LAYOUT_PAIRS | LAYOUT_FX;
+#ifndef VPB_FX_T
+#define VPB_FX_T 42   // target: predicted interval average at 2^T units
+#endif
+#ifndef VPB_FX_P
+#define VPB_FX_P 34   // precision proof: interval sum >= 2^P units per value
+#endif
+constexpr int FX_K_NONE = 1 << 20;   // no prediction (zero or non-finite average)
+// hi + carry(old + lo): the high limb's addend after the low limb's atomic
+// returned `old` (add.cc / addc: one IADD3 with carry out, one IADD.X)
+__device__ __forceinline__ unsigned addc_u32(unsigned hi, unsigned old, unsigned lo) {
+  unsigned h;
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, 0;\n\t}"
+      : "=r"(h)
+      : "r"(old), "r"(lo), "r"(hi));
+  return h;
+}
+// Biased exponent (1023 + k) of an interval's scale 2^k: k = K + e with e the
+// predicted exponent's offset from the base K = 1023 + e0 clamped to
+// [0, 254]; no prediction -> 2^1023 (every normal value goes to the spill).
+__host__ __device__ inline int fx_biased_exp(int k_pred, int e0) {
+  if (k_pred >= FX_K_NONE) return 2046;
+  const int off = k_pred - (e0 - 1023);
+  return e0 + (off < 0 ? 0 : (off > 254 ? 254 : off));
+}
 
 // shared memory of the split layout (per CTA): map rows and histograms of d/2
 // axes, digit table, double-buffered exchange slots and their mbarriers
@@ -225,8 +281,9 @@ __host__ __device__ constexpr bool dq_from_table() {
          D >= 3 && D <= 12 && VPB_TABLE_NT > 0;
 }
 
-template <int ID, int D, int LAYOUT>
+template <int ID, int D, int LAYOUT_>
 __host__ __device__ constexpr int fill_nt() {
+  constexpr int LAYOUT = LAYOUT_ & 7;
   return (LAYOUT == LAYOUT_SPLIT)                    ? VPB_SPLIT_NT
          : dq_from_table<ID, D>()                    ? VPB_TABLE_NT
          : (LAYOUT == LAYOUT_RECORDS && D > 12)      ? VPB_REC_NT
@@ -236,9 +293,13 @@ __host__ __device__ constexpr int fill_nt() {
                                                      : FILL_NT;
 }
 
-template <int ID, int D, int LAYOUT>
-__global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(const FillArgs a) {
-  constexpr int NT = fill_nt<ID, D, LAYOUT>();
+template <int ID, int D, int LAYOUT_>
+__global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(const FillArgs a) {
+  constexpr int NT = fill_nt<ID, D, LAYOUT_>();
+  constexpr int LAYOUT = LAYOUT_ & 7;
+  constexpr bool FX = (LAYOUT_ & LAYOUT_FX) != 0;
+  static_assert(!FX || LAYOUT == LAYOUT_EDGES || LAYOUT == LAYOUT_PAIRS, "FX: edges or pairs");
+  if (a.gate != nullptr && *a.gate == 0) return;   // grid-uniform
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
   constexpr bool SPLIT = LAYOUT == LAYOUT_SPLIT;
   static_assert(!SPLIT || (ID == VPB_GAUSSIAN && D > 0 && D % 2 == 0),
@@ -327,9 +388,28 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
   } else {
     for (int i = tid; i < d * (ng + 1); i += NT) s_edges[i] = a.edges[i];
   }
+  // FX: the scale base K (min over the axes' predicted exponents, clamped so
+  // that every biased exponent 1023 + K + e, e <= 254, is a normal double's)
+  // and each interval's offset e in the top byte of its count word (255: no
+  // prediction -- the scale 2^1023, so every normal value goes to the spill)
+  int fx_e0 = 0;
+  if constexpr (FX) {
+    int K = FX_K_NONE;
+    for (int j = 0; j < d; j++) K = min(K, __ldg(a.fx_kmin + j));
+    K = max(min(K, 1023 - 254), -1022);
+    fx_e0 = 1023 + K;
+  }
   if (a.smem_hist) {
     for (int i = tid; i < hcopies * hs * ng; i += NT) s_hw[i] = 0.0;
-    for (int i = tid; i < hs * ng; i += NT) s_hc[i] = 0u;
+    if constexpr (FX) {
+      for (int i = tid; i < hs * ng; i += NT) {
+        const int b = i / hs, j = i - b * hs;
+        s_hc[i] = j < d ? (unsigned)fx_biased_exp(__ldg(a.fx_k + (size_t)j * ng + b), fx_e0) << 20
+                        : 0u;
+      }
+    } else {
+      for (int i = tid; i < hs * ng; i += NT) s_hc[i] = 0u;
+    }
   }
   if (dq_tab)
     for (int i = tid; i < a.n_strat; i += NT) s_dq[i] = div_exact((double)i, a.nsf, a.rns);
@@ -752,7 +832,52 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
             // 17% slower on cfg2 at round start and still 8% slower after
             // the layout changes: the value-returning CAS costs more
             // shared-memory wavefronts than CAST.SPIN, and wavefronts bind.)
-            {
+            if constexpr (FX) {
+              // fixed point.  Count word = (biased scale exponent << 20) |
+              // count, so the count atomic returns the interval's scale
+              // 2^k as the high word of a double; y = fma(w2, 2^k, 2^52)
+              // holds q = RN(w2 2^k) in its low 52 bits, and (hi:lo) of y is
+              // added to the interval's 64-bit (hi:lo) limbs as it is: the
+              // low limb's atomic returns the old value for the carry, the
+              // high limb gains 0x43300000 per value on top of q's high
+              // bits, which fx_reduce_kernel removes exactly from the count.
+              // No selects, no predicates kept across the axes: one max of
+              // the high words decides the rare spill path, which takes a
+              // too-large value back out (adds 0x43300000:0 - y) and sums it
+              // in f64 in global memory instead.
+              constexpr int DX = D > 0 ? D : 1;
+              unsigned *s_u = reinterpret_cast<unsigned *>(s_hw);
+              unsigned ow[DX], ql[DX], qh[DX];
+#pragma unroll
+              for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_hc[idx[j]], 1u);
+              unsigned mx = 0u;
+#pragma unroll
+              for (int j = 0; j < DX; j++) {
+                const double y =
+                    __fma_rn(w2, __hiloint2double((int)(ow[j] & 0xFFF00000u), 0), 0x1p52);
+                ql[j] = (unsigned)__double2loint(y);
+                qh[j] = (unsigned)__double2hiint(y);
+                mx = max(mx, qh[j]);
+              }
+#pragma unroll
+              for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_u[2 * idx[j]], ql[j]);
+#pragma unroll
+              for (int j = 0; j < DX; j++) atomicAdd(&s_u[2 * idx[j] + 1], addc_u32(qh[j], ow[j], ql[j]));
+              if (mx >= a.fx_lim) {   // rare: q >= 2^L units (or not finite)
+#pragma unroll
+                for (int j = 0; j < DX; j++)
+                  if (qh[j] >= a.fx_lim) {
+                    const unsigned long long nv =
+                        (0x43300000ull << 32) - (((unsigned long long)qh[j] << 32) | ql[j]);
+                    const unsigned nl = (unsigned)nv;
+                    const unsigned o = atomicAdd(&s_u[2 * idx[j]], nl);
+                    atomicAdd(&s_u[2 * idx[j] + 1], addc_u32((unsigned)(nv >> 32), o, nl));
+                    const int b = idx[j] / hs, ax = idx[j] - b * hs;
+                    atomicAdd(a.fx_spill + (size_t)ax * ng + b, w2);
+                    atomicAdd(a.fx_nspill, 1ull);
+                  }
+              }
+            } else {
             // two copies of the sums: the half-warps update different copies,
             // so fewer lanes of one CAS instruction collide on an interval
             double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
@@ -849,6 +974,12 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT>()), 1) fill_kernel(con
     const bool acc = LAYOUT == LAYOUT_RECORDS && a.tile_lo > 0;
     for (int i = tid; i < nh * ng; i += NT) {   // back to [axis][interval]
       const int j = i / ng, b = i - j * ng;
+      if constexpr (FX) {   // the raw (hi:lo) limbs and the count word (with e)
+        reinterpret_cast<unsigned long long *>(hw)[i] =
+            reinterpret_cast<const unsigned long long *>(s_hw)[b * hs + j];
+        hc[i] = s_hc[b * hs + j];
+        continue;
+      }
       double v = s_hw[b * hs + j];
       if (hcopies > 1) v = __dadd_rn(v, s_hw[(size_t)hs * ng + b * hs + j]);
       hw[i] = acc ? __dadd_rn(hw[i], v) : v;

@@ -62,6 +62,8 @@ cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st
   if (a.det) return launch_fill_generic(id, grid, smem, st, a);   // deterministic mode
 #define X(I, D)                                                                  \
   if (id == I && dims == D) {                                                    \
+    if (a.fx && a.pairs) return launch_one<I, D, LAYOUT_PAIRS_FX>(grid, smem, st, a); \
+    if (a.fx) return launch_one<I, D, LAYOUT_EDGES_FX>(grid, smem, st, a);       \
     if (a.records) return launch_one<I, D, LAYOUT_RECORDS>(grid, smem, st, a);   \
     if (a.pairs) return launch_one<I, D, LAYOUT_PAIRS>(grid, smem, st, a);       \
     if (a.smem_hist) return launch_one<I, D, LAYOUT_EDGES>(grid, smem, st, a);   \

@@ -527,10 +527,11 @@ __global__ void fill_fixup_kernel(FillArgs a) {
 // slices in order, then thread p = 0 adds the 8 partials in order.
 __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
                                    long long m, double *map_w, long long *map_counts,
-                                   const int *status) {
+                                   const int *status, const int *gate = nullptr) {
   __shared__ double sw[8][33];
   __shared__ long long sc[8][33];
   if (*status) return;   // failed (now or earlier): the iteration is discarded
+  if (gate != nullptr && *gate == 0) return;   // the fixed-point sums stand (fx_reduce_kernel)
   const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
   const int p = threadIdx.y;
   const int per = (nparts + 7) / 8;
@@ -616,6 +617,117 @@ __global__ void det_convert_kernel(const long long *map_q, const int *bin_k, lon
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m || *status) return;
   map_w[i] = scalbn(__ull2double_rn((unsigned long long)map_q[i]), -bin_k[i]);
+}
+
+// ------------------------------------------------ fixed-point histograms --
+// State of the FX mode (fill.cuh LAYOUT_FX) of one context, device-resident so
+// the captured iteration graph decides by itself which fill runs.
+struct FxState {
+  int gate_fx;    // this iteration's fixed-point fill runs
+  int gate_f64;   // this iteration's f64 fill runs (no prediction, or a redo)
+  int refill;     // set by fx_reduce_kernel: the fixed-point sums failed a proof
+  int fails;      // redone iterations since reset (FX stops after FX_MAX_FAILS)
+  int pred;       // refine_kernel CTAs that wrote a prediction (must be d)
+  int enabled;    // host switch
+  long long n_fx, n_redo;   // statistics: fixed-point iterations, redone ones
+  unsigned long long spills;   // values summed in f64 instead (global, rare)
+};
+constexpr int FX_MAX_FAILS = 3;
+
+// Start of an iteration's fill phase: the fixed-point fill runs when every
+// axis has a prediction from the previous iteration's refinement (not the
+// first refinement from the uniform map: its jump is too large to predict)
+// and FX has not failed too often; otherwise only the f64 fill.
+__global__ void fx_begin_kernel(FxState *fx, const Sched *sched, int dims, const int *status) {
+  const bool use = fx->enabled && fx->pred == dims && sched->it >= 2 &&
+                   fx->fails < FX_MAX_FAILS && *status == 0;
+  fx->gate_fx = use ? 1 : 0;
+  fx->gate_f64 = use ? 0 : 1;
+  fx->refill = 0;
+  fx->pred = 0;
+  if (use) fx->n_fx++;
+}
+
+// Sum of the CTAs' fixed-point slices per interval (exact, 128-bit), the
+// spilled f64 sums added, -> map_w / map_counts; and the proof that decides
+// whether the iteration stands:
+//   * no wrap-around: every value summed is < 2^L units, so a CTA slice with
+//     count c holds < c 2^L; every slice must have c <= 2^(64-L);
+//   * precision: each value rounds by <= 1/2 unit, so an interval with n
+//     values and total S units (fixed point + spill) is within n/2 units,
+//     i.e. 2^-(P+1) relative when S >= 2^P n (e = 255 intervals have no
+//     fixed-point rounding worth the name: scale 2^1023).
+// A failed proof anywhere sets fx->refill and opens the f64 fill (gated
+// second launch in the graph), which recomputes the whole iteration's
+// histograms; its hist_reduce_kernel then overwrites map_w / map_counts.
+__global__ void fx_reduce_kernel(const unsigned long long *hw_part, const unsigned *hc_part,
+                                 int nparts, long long m, int ng, int dims, const int *fx_k,
+                                 const int *fx_kmin,
+                                 int L, double *map_w, long long *map_counts, double *spill,
+                                 FxState *fx, const int *status) {
+  __shared__ unsigned long long s_lo[8][33], s_hi[8][33];
+  __shared__ long long s_c[8][33];
+  __shared__ unsigned s_cm[8][33];
+  __shared__ int s_bad[33];
+  if (!fx->gate_fx || *status) return;
+  const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
+  const int p = threadIdx.y;
+  const int per = (nparts + 7) / 8;
+  const int b0 = p * per, b1 = min(nparts, b0 + per);
+  unsigned long long lo = 0, hi = 0;
+  long long c = 0;
+  unsigned cm = 0;
+  int K = FX_K_NONE;
+  for (int j = 0; j < dims; j++) K = min(K, fx_kmin[j]);
+  const int e0 = 1023 + max(min(K, 1023 - 254), -1022);
+  const unsigned ef = i < m ? (unsigned)fx_biased_exp(fx_k[i], e0) : 0u;
+  bool exp_ok = true;
+  if (i < m) {
+    for (int b = b0; b < b1; b++) {
+      const unsigned w = hc_part[(size_t)b * m + i];
+      // the slice's (hi:lo) minus the 0x43300000 every value added to hi
+      const unsigned long long v =
+          hw_part[(size_t)b * m + i] -
+          ((unsigned long long)((w & 0xFFFFFu) * 0x43300000u) << 32);
+      lo += v;
+      hi += lo < v ? 1ull : 0ull;
+      c += w & 0xFFFFFu;
+      cm = max(cm, w & 0xFFFFFu);
+      exp_ok = exp_ok && (w >> 20) == ef;   // a count past 2^20 would show here
+    }
+  }
+  s_lo[p][threadIdx.x] = lo;
+  s_hi[p][threadIdx.x] = hi;
+  s_c[p][threadIdx.x] = c;
+  s_cm[p][threadIdx.x] = cm;
+  if (p == 0) s_bad[threadIdx.x] = 0;
+  __syncthreads();
+  if (!exp_ok) s_bad[threadIdx.x] = 1;
+  __syncthreads();
+  if (p != 0 || i >= m) return;
+  for (int q = 1; q < 8; q++) {
+    const unsigned long long v = s_lo[q][threadIdx.x];
+    lo += v;
+    hi += (lo < v ? 1ull : 0ull) + s_hi[q][threadIdx.x];
+    c += s_c[q][threadIdx.x];
+    cm = max(cm, s_cm[q][threadIdx.x]);
+  }
+  const int k = (int)ef - 1023;     // the interval's scale 2^k
+  const double units = fma(__ull2double_rn(hi), 0x1p64, __ull2double_rn(lo));
+  const double sp = spill[i];
+  spill[i] = 0.0;
+  map_w[i] = __dadd_rn(scalbn(units, -k), sp);
+  map_counts[i] = c;
+  const bool wrap_free = (double)cm <= ldexp(1.0, 64 - L) && !s_bad[threadIdx.x];
+  const bool precise = c == 0 || ef == 2046u ||
+                       __dadd_rn(units, scalbn(sp, k)) >= ldexp((double)c, VPB_FX_P);
+  if (!(wrap_free && precise)) {
+    if (atomicExch(&fx->refill, 1) == 0) {
+      fx->gate_f64 = 1;
+      fx->fails++;
+      fx->n_redo++;
+    }
+  }
 }
 
 // The exchange's control word, all-reduced with MAX next to the accumulators
@@ -724,7 +836,10 @@ constexpr int REFINE_SMEM_NG = 2048;   // rows up to this length live in smem
 __global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const double *map_w,
                                                           const long long *map_counts, int ng,
                                                           double alpha, double *scratch,
-                                                          int *status, double *damped_out) {
+                                                          int *status, double *damped_out,
+                                                          int *fx_k = nullptr,
+                                                          int *fx_kmin = nullptr,
+                                                          FxState *fx = nullptr) {
   extern __shared__ __align__(16) double rsm[];
   __shared__ BlockPw S;
   __shared__ int s_skip;
@@ -816,6 +931,39 @@ __global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const 
   if (bad) {
     if (threadIdx.x == 0) atomicOr(status, 2);
     return;
+  }
+  if (fx_k != nullptr) {
+    // FX: the next iteration's fixed-point scale per new interval, from the
+    // average w2 of the old interval holding its midpoint, times the change
+    // of this axis's Jacobian factor (w2 carries (ng dx)^2):
+    //   avg' ~ avg_old (dx_new / dx_old)^2,   k = T - ilogb(avg')
+    // so that the interval's values sit near 2^T units (the counts per
+    // interval stay ~n/ng: samples are uniform in y)
+    int kmin = FX_K_NONE;
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) {
+      const double a0 = i == 0 ? e[0] : ne[i], a1 = i == ng - 1 ? e[ng] : ne[i + 1];
+      const double mid = __dadd_rn(a0, __dmul_rn(0.5, __dadd_rn(a1, -a0)));
+      int lo = 0, hi = ng - 1;   // last old interval with e[ob] <= mid
+      while (lo < hi) {
+        const int md = (lo + hi + 1) >> 1;
+        if (e[md] <= mid) lo = md; else hi = md - 1;
+      }
+      const double r = __dadd_rn(a1, -a0) / __dadd_rn(e[lo + 1], -e[lo]);
+      const double pa = d[lo] * r * r;
+      const int k = (pa > 0.0 && isfinite(pa)) ? VPB_FX_T - ilogb(pa) : FX_K_NONE;
+      fx_k[(size_t)j * ng + i] = k;
+      kmin = min(kmin, k);
+    }
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    __shared__ int s_kmin;
+    if (threadIdx.x == 0) s_kmin = FX_K_NONE;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) atomicMin(&s_kmin, kmin);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fx_kmin[j] = s_kmin;
+      atomicAdd(&fx->pred, 1);
+    }
   }
   for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) eg[i] = ne[i];
 }

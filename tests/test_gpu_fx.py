@@ -1,0 +1,98 @@
+"""FX mode: fixed-point interval histograms with predicted scales (fill.cuh
+LAYOUT_FX, update.cuh fx_begin / fx_reduce / refine_kernel's prediction).
+
+The MapWeights sums of vp/kernels.py:100-105 are accumulated per CTA in
+(axis, interval) fixed point instead of f64; fx_reduce_kernel proves every
+interval's sum precise and wrap-free or the iteration's fill is redone in
+f64.  The bar is the reference's, against the CPU oracle (oracle/, the C
+restatement of vp/): evaluations per iteration bitwise, I_it to 1e-10,
+var_it to 1e-8 and the refined map to 1e-12 relative -- with the fixed point
+actually in use (vpb_fx_stats), and through the redo path too.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2408_09229_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+WORKERS = max(1, os.cpu_count() or 1)
+
+# (integrand, dims, n_eval, iterations): the BASELINE integrands at reduced
+# n_eval (same code path, the oracle finishes in seconds) and registry ones
+CASES = [
+    ("multipeak8", 8, 3_000_000, 10),        # cfg2's integrand: pair table, XPERM
+    ("genz_productpeak6", 6, 3_000_000, 8),  # cfg4b: table mode, 1024 threads
+    ("genz_oscillatory6", 6, 3_000_000, 8),  # cfg4a
+    ("ridge", 4, 1_000_000, 6),              # cfg3: edge rows + centre table
+    ("roos_arnold", 10, 2_000_000, 8),       # the paper's workload: stride d = 10
+    ("gaussian", 4, 1_000_000, 10),          # cfg1's narrow peak: predictions miss early
+]
+
+
+def _run(monkeypatch, name, dims, n_eval, its, fx: bool):
+    monkeypatch.setenv("VPB_HIST_FIXED", "1" if fx else "0")
+    bounds = [(0.0, 1.0)] * dims
+    conf = P.IntegratorConfig(n_eval=n_eval, max_it=its, n_intervals=1024)
+    with P.Integrator(name, bounds, conf, device=0) as it:
+        it.iterate(its)
+        est, var, evals = it.history()
+        edges = it.edges()
+        st = it.fx_stats()
+    return np.asarray(est), np.asarray(var), np.asarray(evals), edges, st
+
+
+@pytest.mark.parametrize("name,dims,n_eval,its", CASES, ids=[c[0] for c in CASES])
+def test_fx_trajectory_matches_oracle(monkeypatch, name, dims, n_eval, its):
+    est, var, evals, edges, st = _run(monkeypatch, name, dims, n_eval, its, True)
+    assert st["enabled"]
+    # iterations 0 and 1 are f64 (no prediction yet); every later one starts
+    # in fixed point until FX_MAX_FAILS redos switch it off
+    assert st["fixed_iterations"] >= 1
+    assert st["refilled"] <= min(3, st["fixed_iterations"])
+    bounds = [(0.0, 1.0)] * dims
+    ref = O.integrate(name, bounds, n_eval, max_it=its, n_intervals=1024, workers=WORKERS)
+    np.testing.assert_array_equal(evals, ref.evals)
+    np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
+    np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
+    np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=0.0)
+
+
+@pytest.mark.parametrize("name,dims,n_eval,its", CASES[:3], ids=[c[0] for c in CASES[:3]])
+def test_fx_in_use_on_the_baseline_integrands(monkeypatch, name, dims, n_eval, its):
+    """Every iteration from the third on is filled in fixed point; at most
+    the first of them is redone (the three-peak Gaussian's map still moves
+    by up to 2^8 per interval there), none after."""
+    _, _, _, _, st = _run(monkeypatch, name, dims, n_eval, its, True)
+    assert st["fixed_iterations"] == its - 2, st
+    assert st["refilled"] <= (1 if name == "multipeak8" else 0), st
+
+
+@pytest.mark.parametrize("name,dims,n_eval,its", CASES[:2], ids=[c[0] for c in CASES[:2]])
+def test_fx_matches_f64_histograms(monkeypatch, name, dims, n_eval, its):
+    a = _run(monkeypatch, name, dims, n_eval, its, True)
+    b = _run(monkeypatch, name, dims, n_eval, its, False)
+    assert not b[4]["enabled"]
+    np.testing.assert_array_equal(a[2], b[2])
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-12)
+    np.testing.assert_allclose(a[3], b[3], rtol=1e-13, atol=0.0)
+
+
+def test_fx_default_policy(monkeypatch):
+    """On by default from 1e7 evaluations per iteration where eligible; off
+    below, in deterministic mode and for the generic kernel."""
+    monkeypatch.delenv("VPB_HIST_FIXED", raising=False)
+    conf = P.IntegratorConfig(n_eval=10 ** 7, max_it=1, n_intervals=1024)
+    with P.Integrator("multipeak8", [(0.0, 1.0)] * 8, conf, device=0) as it:
+        assert it.fx_stats()["enabled"]
+    conf = P.IntegratorConfig(n_eval=10 ** 6, max_it=1, n_intervals=1024)
+    with P.Integrator("multipeak8", [(0.0, 1.0)] * 8, conf, device=0) as it:
+        assert not it.fx_stats()["enabled"]
+    monkeypatch.setenv("VPB_HIST_FIXED", "1")
+    conf = P.IntegratorConfig(n_eval=10 ** 6, max_it=1, n_intervals=1024)
+    with P.Integrator("gaussian", [(0.0, 1.0)] * 5, conf, device=0) as it:   # generic kernel
+        assert not it.fx_stats()["enabled"]

@@ -3,6 +3,6 @@
 CFGS=$1; shift
 for c in $CFGS; do
   for e in "" "$@"; do
-    env $e timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', '${e:-default}', '%.3e'%d['value'], 'frac %.3f'%d['roofline']['frac'], 'fill_ms %.3f'%d['roofline']['fill_kernel_ms_per_step'])"
+    env $e timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', '${e:-default}', '%.3e'%d['value'], 'frac %.3f'%d['roofline']['frac'], 'fill_ms %.3f'%d['roofline']['fill_kernel_ms_per_step'], d.get('histograms'))"
   done
 done

@@ -94,6 +94,35 @@ __global__ void __launch_bounds__(NT, 1) histk(double *out, int evals, int ng, i
       } else if (MODE == 8) {   // POPC count only
 #pragma unroll
         for (int s = 0; s < D; s++) atomicAdd(&cnt[idx[s]], 1u);
+      } else if (MODE == 10 || MODE == 11) {
+        // the fill's fixed-point design: per-bin scale exponent in the count
+        // word's top byte (MODE 10: count atomic returns it) or per-axis in a
+        // register (MODE 11: POPC count); q = RN(w2 2^k) by one DFMA against
+        // 2^52; u32 lo limb with return, hi limb gets q_hi + carry
+        unsigned ex[D];
+        if (MODE == 10) {
+#pragma unroll
+          for (int s = 0; s < D; s++) ex[s] = atomicAdd(&cnt[idx[s]], 1u) >> 24;
+        } else {
+#pragma unroll
+          for (int s = 0; s < D; s++) { atomicAdd(&cnt[idx[s]], 1u); ex[s] = (unsigned)s; }
+        }
+        unsigned ql[D], qh[D];
+#pragma unroll
+        for (int s = 0; s < D; s++) {
+          const double sc = __hiloint2double((int)((1023u + 40u + ex[s]) << 20), 0);
+          const double y = __fma_rn(w2, sc, 0x1p52);
+          ql[s] = (unsigned)__double2loint(y);
+          qh[s] = (unsigned)__double2hiint(y);
+        }
+        unsigned old[D];
+#pragma unroll
+        for (int s = 0; s < D; s++) old[s] = atomicAdd(&hi32[idx[s]], ql[s]);
+#pragma unroll
+        for (int s = 0; s < D; s++) {
+          const unsigned c = old[s] + ql[s] < ql[s] ? 1u : 0u;
+          atomicAdd(&((unsigned *)hi)[idx[s]], (qh[s] & 0xFFFFFu) + c);
+        }
       } else if (MODE == 9) {   // u32 limb with return + carry-conditional second limb + count
         unsigned old[D];
 #pragma unroll
@@ -153,6 +182,10 @@ int main() {
     run<7, 8, 768>("2x u32 ADD limbs + POPC count", 1024, 205, sms, clk, out);
     run<8, 8, 768>("POPC count only", 1024, 205, sms, clk, out);
     run<9, 8, 768>("u32 limb(ret) + carry limb + POPC", 1024, 205, sms, clk, out);
+    run<10, 8, 768>("fixed design: cnt(ret,exp) dfma lo(ret) hi", 1024, 205, sms, clk, out);
+    run<11, 8, 768>("fixed design: POPC, axis exp, lo(ret) hi", 1024, 205, sms, clk, out);
+    run<10, 6, 1024>("fixed design: cnt(ret,exp) dfma lo(ret) hi", 1024, 102, sms, clk, out);
+    run<11, 6, 1024>("fixed design: POPC, axis exp, lo(ret) hi", 1024, 102, sms, clk, out);
     run<5, 6, 1024>("u32 ATOMS.ADD value x1", 1024, 102, sms, clk, out);
     run<7, 6, 1024>("2x u32 ADD limbs + POPC count", 1024, 102, sms, clk, out);
     run<8, 6, 1024>("POPC count only", 1024, 102, sms, clk, out);
