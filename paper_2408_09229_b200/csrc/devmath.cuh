@@ -84,23 +84,53 @@ __device__ __forceinline__ double div_exact(double a, double b, double r) {
 //    integer domain and converted back exactly with the same shifter.
 // dq = RN(digit/N); nsf2 = 2N; rns2 = RN(1/N)/2; edge(iv, lo, dx) returns
 // E[j][iv] and RN(E[j][iv+1] - E[j][iv]) of the axis.
+// VPB_A_I2F: 2u as the integer w >> 11 converted exactly (I2F.F64.U64), the
+// Markstein constants scaled by 2^52 / 2^-52 (sample_consts) -- the same
+// quotient bits, three integer instructions fewer per axis than the bit
+// assembly below.
+#ifndef VPB_A_I2F
+#define VPB_A_I2F 1   // measured: cfg2 fill -2.8%, cfg4b -2.6%
+#endif
+// VPB_YCLAMP_DMNMX: the y >= 1 clamp as fmin against 0x1.fffffffffffffp-1
+// (y >= 0, never NaN: the same bits) instead of three integer instructions
+// on the high/low words -- measured no better: sm_100a has no FP64 min
+// instruction, fmin is DSETP.MIN + two selects.
+#ifndef VPB_YCLAMP_DMNMX
+#define VPB_YCLAMP_DMNMX 0
+#endif
+// (2N, RN(1/N)/2) for sample_axis's u/N = 2u/(2N), in the scaling its 2u uses
+__host__ __device__ inline void sample_consts(double nsf, double rns, double &nsf2,
+                                              double &rns2) {
+  nsf2 = VPB_A_I2F ? nsf * 0x1p53 : 2.0 * nsf;
+  rns2 = VPB_A_I2F ? rns * 0x1p-53 : 0.5 * rns;
+}
+// first: the run's first axis (a constant after unrolling) -- jac = its
+// factor instead of RN(1 * factor), the same bits
 template <class EdgeFn>
 __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2, double rns2,
                                               double ngf, int ng, EdgeFn edge, double &jac,
-                                              int &iv) {
+                                              int &iv, bool first = false) {
+#if VPB_A_I2F
+  const double a = __ull2double_rn(w >> 11);   // 2u * 2^52, exact (< 2^53)
+#else
   uint32_t whi, wlo;   // split opaquely: keeps the bit-63 test a 32-bit compare
   asm("mov.b64 {%0, %1}, %2;" : "=r"(wlo), "=r"(whi) : "l"(w));
   const double up = __hiloint2double((int)(((whi >> 11) & 0xFFFFFu) | 0x3FF00000u),
                                      (int)__funnelshift_r(wlo, whi, 11));
   const double cm = __hiloint2double((~(int)whi >> 31) & 0x3FF00000, 0);   // 1 - bit63
   const double a = __dadd_rn(up, -cm);                                      // 2u, exact
+#endif
   const double q0 = __dmul_rn(a, rns2);                                     // Markstein
   const double v = __fma_rn(__fma_rn(-q0, nsf2, a), rns2, q0);             // RN(u/N)
   const double ys = __dadd_rn(dq, v);
+#if VPB_YCLAMP_DMNMX
+  const double t = __dmul_rn(fmin(ys, 0x1.fffffffffffffp-1), ngf);
+#else
   int yhi = __double2hiint(ys), ylo = __double2loint(ys);
   ylo = (yhi >= 0x3FF00000) ? -1 : ylo;                                     // y >= 1 ->
   yhi = min(yhi, 0x3FEFFFFF);                                               // 0x3FEFFFFFFFFFFFFF
   const double t = __dmul_rn(__hiloint2double(yhi, ylo), ngf);
+#endif
   const double sh = __dadd_rz(t, 4503599627370496.0);   // 2^52 + trunc(t)
   const int ivj = min(__double2loint(sh), ng - 1);
   // 2^52 + iv has the shifter's high word (0x43300000): reuse that register
@@ -108,7 +138,7 @@ __device__ __forceinline__ double sample_axis(uint64_t w, double dq, double nsf2
   const double frac = __dadd_rn(t, -fiv);
   double elo, dx;
   edge(ivj, elo, dx);
-  jac = __dmul_rn(jac, __dmul_rn(ngf, dx));
+  jac = first ? __dmul_rn(ngf, dx) : __dmul_rn(jac, __dmul_rn(ngf, dx));
   iv = ivj;
   return __dadd_rn(elo, __dmul_rn(frac, dx));
 }

@@ -442,7 +442,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   const int xr = XPERM ? (lane & (D - 1)) : 0;   // XPERM: step s samples axis s ^ xr
-  const double nsf2 = 2.0 * a.nsf, rns2 = 0.5 * a.rns;   // u/N = (2u)/(2N), exact scaling
+  double nsf2, rns2;   // u/N = (2u)/(2N), exact scaling
+  sample_consts(a.nsf, a.rns, nsf2, rns2);
   // this warp's tiles: [L + w*P + b, min(L + (w+1)*P, U)) in steps of the grid,
   // [L, U) = the launch's tile range
   const long long tL = a.tile_lo, tU = min(a.tile_hi, ntiles);
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
                      w0, w1);
             }
             x[jl] = sample_axis((jl & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
-                                EdgeRow{s_edges + jl * (ng + 1)}, jac, iv[jl]);
+                                EdgeRow{s_edges + jl * (ng + 1)}, jac, iv[jl], jl == 0);
             const double u = __dadd_rn(x[jl], -a.P.p[0]);   // (x_j - mu)^2, this half
             gacc[0].add(jl, __dmul_rn(u, u));
           }
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             const double dq0 = DQ_REG ? dq[DQ_REG ? s0 : 0] : dq_of(s0 ^ xr);
             const double dq1 = DQ_REG ? dq[DQ_REG ? s1 : 0] : dq_of(s1 ^ xr);
             x[s0] = sample_axis(wa, dq0, nsf2, rns2, a.ngf, ng,
-                                EdgePairsT<D>{s_pair + (s0 ^ xr)}, jac, iv[s0]);
+                                EdgePairsT<D>{s_pair + (s0 ^ xr)}, jac, iv[s0], k2 == 0);
             x[s1] = sample_axis(wb, dq1, nsf2, rns2, a.ngf, ng,
                                 EdgePairsT<D>{s_pair + (s1 ^ xr)}, jac, iv[s1]);
             stream_axis(s0, x[s0]);
@@ -636,10 +637,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
           }
           if constexpr (PAIRS)
             x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
-                               EdgePairs{s_pair + j * ng}, jac, iv[j]);
+                               EdgePairs{s_pair + j * ng}, jac, iv[j], j == 0);
           else
             x[j] = sample_axis((j & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
-                               EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j]);
+                               EdgeRow{s_edges + j * (ng + 1)}, jac, iv[j], j == 0);
           stream_axis(j, x[j]);
           if constexpr (LAYOUT == LAYOUT_RECORDS) {
             // the axis group is complete: store its intervals now, so they

@@ -1020,6 +1020,8 @@ __global__ void sample_runs_kernel(unsigned long long seed, long long batch, lon
   const unsigned long long sl = g % (unsigned long long)batch, k = g / (unsigned long long)batch;
   const unsigned long long base = k * (unsigned long long)((dims + (dims & 1)) >> 1);
   const double nsf = (double)n_strat, rns = 1.0 / nsf, ngf = (double)ng;
+  double nsf2, rns2;
+  sample_consts(nsf, rns, nsf2, rns2);
   long long rem = c;
   double jf = 1.0;
   uint64_t w0 = 0, w1 = 0;
@@ -1031,8 +1033,8 @@ __global__ void sample_runs_kernel(unsigned long long seed, long long batch, lon
     const long long q = rem / n_strat, dig = rem - q * n_strat;
     rem = q;
     int iv;
-    x[i * dims + j] = sample_axis((j & 1) ? w1 : w0, div_exact((double)dig, nsf, rns), 2.0 * nsf,
-                                  0.5 * rns, ngf, ng, EdgeRow{edges + (size_t)j * (ng + 1)}, jf, iv);
+    x[i * dims + j] = sample_axis((j & 1) ? w1 : w0, div_exact((double)dig, nsf, rns), nsf2,
+                                  rns2, ngf, ng, EdgeRow{edges + (size_t)j * (ng + 1)}, jf, iv);
     idx[i * dims + j] = iv;
   }
   jac[i] = jf;
