@@ -273,9 +273,13 @@ __host__ __device__ constexpr bool axis_symmetric() {
 #ifndef VPB_TABLE_RIDGE
 #define VPB_TABLE_RIDGE 1   // cfg3 -0.4%
 #endif
+#ifndef VPB_TABLE_MULTIPEAK
+#define VPB_TABLE_MULTIPEAK 0
+#endif
 template <int ID, int D>
 __host__ __device__ constexpr bool dq_from_table() {
   return (ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_ROOS_ARNOLD ||
+          (ID == VPB_MULTIPEAK && VPB_TABLE_MULTIPEAK) ||
           ID == VPB_LINEAR || ID == VPB_EXPONENTIAL || ID == VPB_MOROKOFF ||
           ID == VPB_PATH_INTEGRAL || (ID == VPB_RIDGE && VPB_TABLE_RIDGE)) &&
          D >= 3 && D <= 12 && VPB_TABLE_NT > 0;

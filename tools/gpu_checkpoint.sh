@@ -5,10 +5,12 @@
 TAG=${1:-ck}
 mkdir -p gpurun_out/$TAG
 # DRAM bytes of one fill launch per config (roofline.traffic; base units)
+# (the working fill of iteration 5: the fixed-point one where FX is on)
 for c in cfg1 cfg2 cfg3 cfg4a cfg4b cfg5 ra10; do
+  RX=$(python tools/profile_fill.py $c 5 --probe)
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum \
-    --print-units base --clock-control none --csv -k regex:fill_kernel -s 2 -c 1 \
-    --log-file gpurun_out/$TAG/traffic_$c.csv python tools/profile_fill.py $c 3 > /dev/null 2>&1
+    --print-units base --clock-control none --csv --profile-from-start off --kernel-name-base mangled \
+    -k "regex:$RX" --log-file gpurun_out/$TAG/traffic_$c.csv python tools/profile_fill.py $c 5 > /dev/null 2>&1
   echo "traffic $c rc=$?"
 done
 # instruction counts into profiles/fill_traffic.json before the bench lines
@@ -26,5 +28,7 @@ bash tools/gpu_profile.sh cfg2 $TAG/p
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/$TAG/p_launches_cfg1.csv python bench.py --config cfg1 --steps 3 --warmup 3 --no-cpu \
   > /dev/null 2>&1; echo "cfg1 launches rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 2 -c 1 \
-  -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 4 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
+RX=$(python tools/profile_fill.py cfg4b 5 --probe)
+timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
+  --kernel-name-base mangled -k "regex:$RX" -c 1 \
+  -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 5 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
