@@ -246,6 +246,54 @@ def run_reference(args, cfgname, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def per_function_loop(cfg, n_eval, warmup, steps):
+    """vp/core.py:200-219 with every function replaced by its C entry point
+    (ops.py: build_run_plan, parallel_fill -> vpb_fill_host, compute_results,
+    update_evals_per_cube, smooth_and_damp, update_grid), host numpy arrays
+    in and out; wall clock per iteration, host<->device bytes counted from
+    the arrays each call moves."""
+    import numpy as np
+
+    from paper_2408_09229_b200 import ops
+    from paper_2408_09229_b200.core import compute_n_strat
+    dims, ng = cfg["dims"], cfg["ng"]
+    ns = compute_n_strat(n_eval, dims)
+    edges = np.tile(np.linspace(0.0, 1.0, ng + 1), (dims, 1))
+    n_h = ops.update_evals_per_cube(np.zeros(ns ** dims), 0.0, n_eval)
+    run_base, seed, batch = 0, 0, 1 << 20
+    times, evals, h2d, d2h = [], 0, 0, 0
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        off = ops.build_run_plan(n_h)
+        mw, mc, s1, s2, cnt = ops.parallel_fill(off, edges, ns, seed, batch, cfg["integrand"],
+                                                run_base)
+        i_it, v_it, d_h = ops.compute_results(s1, s2, cnt)
+        n_h = ops.update_evals_per_cube(d_h, 0.75, n_eval)
+        edges = ops.update_grid(edges, ops.smooth_and_damp(mw, mc, 0.5))
+        t1 = time.perf_counter()
+        total = int(off[-1])
+        run_base += total
+        if it >= warmup:
+            times.append(t1 - t0)
+            evals += total
+            # fill: offsets + edges in; map (f64 + i64) and s1, s2 out;
+            # results: s1, s2, counts in, d_h out; allocation: d_h in, n_h
+            # out; plan: n_h in, offsets out; damp + grid: map in, damped
+            # out, edges + damped in, edges out
+            nc = ns ** dims
+            h2d += 8 * (nc + 1) + 8 * edges.size + 24 * nc + 8 * nc + 8 * nc + 16 * mw.size \
+                + 8 * edges.size + 8 * mw.size
+            d2h += 16 * mw.size + 16 * nc + 8 * nc + 8 * nc + 8 * (nc + 1) + 8 * mw.size \
+                + 8 * edges.size
+    t = sum(times)
+    return {"value": evals / t, "unit": UNIT, "ms_per_step": 1e3 * t / len(times),
+            "steps": len(times), "h2d_bytes_per_step": h2d // len(times),
+            "d2h_bytes_per_step": d2h // len(times),
+            "path": "ops.build_run_plan -> ops.parallel_fill (vpb_fill_host, cached context) "
+                    "-> ops.compute_results -> ops.update_evals_per_cube -> "
+                    "ops.smooth_and_damp -> ops.update_grid, host numpy buffers, wall clock"}
+
+
 def run_gpu(args, cfgname, cfg, world, rank, local):
     import numpy as np
     import torch
@@ -318,6 +366,14 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
     d2h = pinned_out.nbytes + 8 + 8 + 8
     e_integ.close()
 
+    # ---- the per-function binding: the reference's own
+    # iteration loop kept in the host language, each function on the path a
+    # stateless C call with host buffers (ops.py = the ctypes stub), so the
+    # plan offsets, the map and the accumulators cross PCIe every iteration
+    per_function = None
+    if world == 1 and not args.no_per_function:
+        per_function = per_function_loop(cfg, n_eval, warmup, min(steps, 5))
+
     layout = integ.fill_layout()
     fx = integ.fx_stats()
     fx["mode"] = "fixed point (per-interval predicted scale)" if fx["enabled"] else "f64 CAS"
@@ -384,6 +440,7 @@ def run_gpu(args, cfgname, cfg, world, rank, local):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
+            "per_function_binding": per_function,
             "gpu_launches": layout["launches_per_iteration"] * steps,
             "clocks": clk,
             "estimates": {"last": float(est[-1]), "sigma_last": float(np.sqrt(var[-1]))},
@@ -402,6 +459,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-per-function", action="store_true",
+                    help="skip the per-function-binding measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: n_eval per GPU; strong: n_eval in total (default: strong for "

@@ -1646,15 +1646,41 @@ int vpb_fill_host(const int64_t *offsets, int64_t n_cubes, const double *edges, 
     bnds[2 * j] = edges[(size_t)j * (ng + 1)];
     bnds[2 * j + 1] = edges[(size_t)j * (ng + 1) + ng];
   }
-  vpb_desc d{};
-  d.dims = dims; d.n_intervals = ng; d.n_strat = n_strat;
-  d.n_eval = std::max<long long>(4, total);
-  d.batch_size = batch; d.seed = seed; d.alpha = 0.5; d.beta = 0.75;
-  d.integrand = integrand; d.n_params = n_params; d.params = params; d.bounds = bnds.data();
-  d.device = -1; d.max_it = 1; d.stream = nullptr;
-  vpb_ctx *c = nullptr;
-  TRY(vpb_create(&d, &c));
-  struct Guard { vpb_ctx *c; ~Guard() { vpb_destroy(c); } } guard{c};
+  // One cached context per process, reused while the geometry, integrand,
+  // parameters, Philox stream (seed, batch) and device match and the plan
+  // fits its buffers: the reference calls parallel_fill once per iteration
+  // with the same configuration, so only the first call pays the context's
+  // creation (buffers, events, the graph-less stream).  Calls serialise on
+  // the cache's mutex.  The cached context is never destroyed (a static
+  // destructor would run after the CUDA runtime's teardown).
+  static std::mutex cache_mu;
+  static vpb_ctx *cache = nullptr;
+  static std::vector<double> cache_params;
+  std::lock_guard<std::mutex> lock(cache_mu);
+  int cur_dev = 0;
+  CK(cudaGetDevice(&cur_dev));
+  const std::vector<double> pv(params, params + n_params);
+  const bool hit = cache && cache->dims == dims && cache->ng == ng && cache->ns == n_strat &&
+                   cache->id == integrand && cache->seed == seed && cache->batch == batch &&
+                   cache->dev == cur_dev && cache_params == pv && cache->bounds == bnds &&
+                   (total + 2 * nc) / FILL_TILE + 2 <= cache->ntiles_cap;
+  vpb_ctx *c = cache;
+  if (!hit) {
+    if (cache) { vpb_destroy(cache); cache = nullptr; }
+    vpb_desc d{};
+    d.dims = dims; d.n_intervals = ng; d.n_strat = n_strat;
+    d.n_eval = std::max<long long>(4, total + total / 4);   // headroom for later plans
+    d.batch_size = batch; d.seed = seed; d.alpha = 0.5; d.beta = 0.75;
+    d.integrand = integrand; d.n_params = n_params; d.params = params; d.bounds = bnds.data();
+    d.device = -1; d.max_it = 1; d.stream = nullptr;
+    TRY(vpb_create(&d, &c));
+    cache = c;
+    cache_params = pv;
+  } else {
+    TRY(setdev(c));
+    CK(cudaMemsetAsync(c->status, 0, sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->err_run, 0xFF, sizeof(unsigned long long), c->st));
+  }
   TRY(vpb_set_edges(c, edges));
   std::vector<int64_t> nh(n_cubes);
   for (long long h = 0; h < n_cubes; h++) nh[h] = offsets[h + 1] - offsets[h];
