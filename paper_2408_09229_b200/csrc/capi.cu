@@ -292,6 +292,12 @@ struct vpb_ctx {
   long long *map_q = nullptr;   // [d*ng] pass-2 fixed-point sums
   // FX mode (fill.cuh LAYOUT_FX): fixed-point interval histograms with
   // predicted scales, proven by fx_reduce_kernel or redone in f64
+  // cooperative post-fill update (update_coop_kernel): one launch instead of
+  // the fixup/reduce/results/allocation/refinement chain (single GPU)
+  bool coop = false;
+  int coop_grid = 0;
+  size_t coop_smem = 0;
+  unsigned *coop_bar = nullptr;
   bool fx = false;
   int fx_L = 52;                // values below 2^L units are summed in fixed point
   FxState *fxs = nullptr;
@@ -482,7 +488,7 @@ int host_exchange(vpb_ctx *c) {
 // whole plan (world 1): every cube has >= 1 run and the fill / fixup assign
 // (never accumulate) each cube's sums exactly once.
 int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k1 = nullptr,
-                 bool defer_join = false, bool zero_cubes = true) {
+                 bool defer_join = false, bool zero_cubes = true, bool post = true) {
   const size_t m = (size_t)c->dims * c->ng;
   if (zero_cubes) CK(cudaMemsetAsync(c->s1, 0, sizeof(double) * 2 * c->n_cubes, c->st));
   if (!c->smem_hist && !c->records) {
@@ -568,6 +574,7 @@ int enqueue_fill(vpb_ctx *c, bool timed, cudaEvent_t k0 = nullptr, cudaEvent_t k
   }
   if (k1) CK(rec_event(c, k1));
   if (timed) CK(cudaEventRecord(c->f1, c->st));
+  if (!post) return VPB_OK;   // the cooperative update kernel does the rest
   const long long nt = c->ntiles_cap;
   TRY(fork_side(c));   // histogram reduction (side) || cube-chain fixup (st)
   fill_fixup_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, c->st>>>(a);
@@ -671,7 +678,77 @@ __global__ void end_iteration_kernel(const int *status, int *fail_it, Sched *sch
   }
 }
 
+#ifndef VPB_COOP_ATTR
+#define VPB_COOP_ATTR 1
+#endif
+int enqueue_update_coop(vpb_ctx *c) {
+  UpdArgs u{};
+  u.fa = fill_args(c);
+  u.hw_part = c->hw_part;
+  u.hc_part = c->hc_part;
+  u.nparts = c->grid_tiles;
+  u.m = (long long)c->dims * c->ng;
+  u.map_w = c->map_w;
+  u.map_counts = c->map_counts;
+  u.hist_gate = c->fx ? &c->fxs->gate_f64 : nullptr;
+  u.edges = c->edges;
+  u.ng = c->ng;
+  u.dims = c->dims;
+  u.alpha = c->alpha;
+  u.refine_scr = c->refine_scr;
+  u.fx_k = c->fx ? c->fx_k : nullptr;
+  u.fx_kmin = c->fx_kmin;
+  u.fxs = c->fxs;
+  u.s1 = c->s1;
+  u.s2 = c->s2;
+  u.offsets = c->offsets;
+  u.n_cubes = c->n_cubes;
+  u.V = 1.0 / (double)c->n_cubes;
+  u.beta = c->beta;
+  u.d_h = c->d_h;
+  u.dp = c->dp;
+  u.pw = c->pw.dev();
+  u.pwvals = c->pwvals;
+  u.pwterms = c->pwterms;
+  u.sc = c->sc;
+  u.h_est = c->h_est;
+  u.h_var = c->h_var;
+  u.sched = c->sched;
+  u.record = 1;
+  u.tree_flags = pw_tree_flags(u.pw);
+  u.ne = (double)c->n_eval;
+  u.uniform_nh = c->uniform_nh;
+  u.n_h = c->n_h;
+  u.bsum = c->bsum;
+  u.nb = c->nb;
+  u.status = c->status;
+  u.fail_it = c->fail_it;
+  u.bar = c->coop_bar;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)c->coop_grid);
+  cfg.blockDim = dim3(UPD_NT);
+  cfg.dynamicSmemBytes = c->coop_smem;
+  cfg.stream = c->st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = VPB_COOP_ATTR ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, update_coop_kernel, u));
+  return VPB_OK;
+}
+
 int enqueue_iteration_body(vpb_ctx *c, std::array<cudaEvent_t, 6> &E) {
+  if (c->coop) {
+    CK(rec_event(c, E[0]));
+    TRY(enqueue_plan(c, 1, nullptr));
+    CK(rec_event(c, E[1]));
+    TRY(enqueue_fill(c, false, E[2], E[3], false, false, /*post=*/false));
+    CK(rec_event(c, E[4]));
+    TRY(enqueue_update_coop(c));
+    CK(rec_event(c, E[5]));
+    return VPB_OK;
+  }
   CK(rec_event(c, E[0]));
   TRY(enqueue_plan(c, 1, nullptr));
   CK(rec_event(c, E[1]));
@@ -770,7 +847,8 @@ void free_ctx(vpb_ctx *c) {
                   c->ck_head, c->ck_tail, c->cv_head, c->cv_tail, c->ct_through, c->hw_part,
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec,
-                  c->ctl, c->bin_k, c->map_q, c->fxs, c->fx_k, c->fx_kmin, c->fx_spill};
+                  c->ctl, c->bin_k, c->map_q, c->fxs, c->fx_k, c->fx_kmin, c->fx_spill,
+                  c->coop_bar};
   for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
@@ -1055,6 +1133,32 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
       A(c->fx_spill, m);
     }
   }
+  // cooperative update kernel (opt-in, VPB_COOP=1): single GPU,
+  // shared-memory histograms (not records), not deterministic; one
+  // 1024-thread CTA per SM must be resident with the larger of the
+  // refinement's and the pairwise tree's shared memory, and the refinement
+  // CTAs (one per axis) must leave CTAs for the rest.  Measured slower than
+  // the launch chain on cfg1 (0.166 vs 0.160 ms per iteration),
+  // so the chain stays the default.
+  {
+    c->coop_smem = update_coop_smem(c->ng, c->pw.dev());
+    cudaFuncAttributes fa{};
+    const char *ce = std::getenv("VPB_COOP");
+    bool ok = !c->det && !c->records && c->smem_hist && ce && ce[0] == '1' &&
+              c->dims + 1 < sms &&
+              cudaFuncGetAttributes(&fa, update_coop_kernel) == cudaSuccess &&
+              c->coop_smem + fa.sharedSizeBytes <= (size_t)optin;
+    int per_sm = 0;
+    if (ok)
+      ok = cudaFuncSetAttribute(update_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)c->coop_smem) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, update_coop_kernel, UPD_NT,
+                                                         c->coop_smem) == cudaSuccess &&
+           per_sm >= 1;
+    c->coop = ok;
+    c->coop_grid = sms;
+    if (c->coop) A(c->coop_bar, 5);
+  }
   if (c->records) {
     c->n_groups = (c->dims - c->rec_k0 + 7) / 8;
     const long long cap_runs = c->ntiles_cap * FILL_TILE;
@@ -1154,6 +1258,7 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
   if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
   if (c->exch_fn) return fail(VPB_ERR_INVALID, "context already has a host exchange");
   NK(ncclCommInitRank(&c->comm, world, uid, rank));
+  c->coop = false;   // the exchange sits between the reduction and the update
   c->world = world;
   c->rank = rank;
   shard_chunks(c);
@@ -1162,6 +1267,7 @@ int vpb_attach_nccl(vpb_ctx *c, const char id[128], int32_t world, int32_t rank)
 
 int vpb_set_shard(vpb_ctx *c, int32_t world, int32_t rank) {
   if (world < 1 || rank < 0 || rank >= world) return fail(VPB_ERR_INVALID, "bad world/rank");
+  if (world > 1) c->coop = false;   // shards need zeroed cube sums and a merge
   c->world = world;
   c->rank = rank;
   shard_chunks(c);
@@ -1188,6 +1294,7 @@ int vpb_attach_exchange(vpb_ctx *c, int32_t world, int32_t rank, vpb_allreduce_f
   if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
   if (c->graph) { cudaGraphDestroy(c->graph); c->graph = nullptr; }
   c->use_graph = false;
+  c->coop = false;
   c->exch_fn = fn;
   c->exch_user = user;
   c->world = world;
@@ -1211,6 +1318,7 @@ int vpb_reset(vpb_ctx *c) {
   unsigned long long big = ~0ull;
   CK(cudaMemcpy(c->err_run, &big, sizeof(big), cudaMemcpyHostToDevice));
   CK(cudaMemset(c->h_evals, 0, sizeof(long long) * c->max_it));
+  if (c->coop) CK(cudaMemset(c->coop_bar, 0, sizeof(unsigned) * 5));
   if (c->fx) {
     FxState f{};
     f.enabled = 1;
@@ -1348,7 +1456,8 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   const int n_rec = c->dims - c->rec_k0;
   const int fill = c->records ? c->n_chunks * (1 + (n_rec >= 8) + (n_rec % 8 != 0)) : 1;
   if (launches)
-    *launches = 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1 + (c->fx ? 3 : 0);
+    *launches = c->coop ? 2 + fill + 1 + (c->fx ? 3 : 0)
+                        : 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1 + (c->fx ? 3 : 0);
   return VPB_OK;
 }
 

@@ -77,11 +77,9 @@ __global__ void cube_terms_kernel(const double *s1, const double *s2, const long
   terms[2 * n + h] = p;
 }
 
-__global__ void results_leaf_kernel(const double *terms, long long n, PwPlanDev pw, double *vals,
-                                    const int *status) {
-  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void results_leaf_body(long long gt, const double *terms, long long n, PwPlanDev pw,
+                                  double *vals) {
   const int leaf = (int)(gt >> 3), j = (int)(gt & 7);
-  if (*status & 1) return;
   const bool live = leaf < pw.L;
   const long long o = live ? pw.leaf_off[leaf] : 0;
   const int len = live ? pw.leaf_len[leaf] : 0;
@@ -109,6 +107,12 @@ __global__ void results_leaf_kernel(const double *terms, long long n, PwPlanDev 
   vals[3 * leaf + 0] = rm;
   vals[3 * leaf + 1] = rt;
   vals[3 * leaf + 2] = rp;
+}
+
+__global__ void results_leaf_kernel(const double *terms, long long n, PwPlanDev pw, double *vals,
+                                    const int *status) {
+  if (*status & 1) return;
+  results_leaf_body((long long)blockIdx.x * blockDim.x + threadIdx.x, terms, n, pw, vals);
 }
 
 // Generic leaf kernel for a plain array (parity entry point vpb_pairwise_sum).
@@ -189,11 +193,9 @@ struct Scalars {
 };
 
 // Finishes compute_results (vp/strat.py:205-207) and records the history.
-__global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, double V,
-                                    Scalars *sc, double *hist_est, double *hist_var,
-                                    Sched *sched, const int *status, int record, int flags) {
-  extern __shared__ __align__(16) unsigned char tree_sm[];
-  if (*status & 1) return;
+__device__ void results_tree_body(unsigned char *tree_sm, PwPlanDev pw, double *vals, long long n,
+                                  double V, Scalars *sc, double *hist_est, double *hist_var,
+                                  Sched *sched, int record, int flags) {
   pw_tree_combine(pw, vals, tree_sm, flags);
   if (threadIdx.x == 0) {
     const int root = pw.I > 0 ? pw.L + pw.I - 1 : 0;
@@ -209,6 +211,14 @@ __global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, dou
   }
 }
 
+__global__ void results_tree_kernel(PwPlanDev pw, double *vals, long long n, double V,
+                                    Scalars *sc, double *hist_est, double *hist_var,
+                                    Sched *sched, const int *status, int record, int flags) {
+  extern __shared__ __align__(16) unsigned char tree_sm[];
+  if (*status & 1) return;
+  results_tree_body(tree_sm, pw, vals, n, V, sc, hist_est, hist_var, sched, record, flags);
+}
+
 __global__ void array_tree_kernel(PwPlanDev pw, double *vals, double *out) {
   pw_tree_combine(pw, vals);
   if (threadIdx.x == 0) *out = vals[3 * (pw.I > 0 ? pw.L + pw.I - 1 : 0)];
@@ -219,12 +229,12 @@ __global__ void array_tree_kernel(PwPlanDev pw, double *vals, double *out) {
 // or total <= 0 (vp/strat.py:101-113).  Also the per-block sums for the plan.
 constexpr int PLAN_NT = 1024;
 
-__global__ void alloc_kernel(const double *dp, long long n, double beta, double ne,
-                             long long uniform_nh, const Scalars *sc, int use_uniform,
-                             long long *n_h, long long *bsum, const int *status) {
+// One PLAN_NT-cube block vb of the allocation (a PLAN_NT-thread block).
+__device__ void alloc_block(long long vb, const double *dp, long long n, double beta, double ne,
+                            long long uniform_nh, const Scalars *sc, int use_uniform,
+                            long long *n_h, long long *bsum) {
   __shared__ long long red[PLAN_NT / 32];
-  if (*status & 1) return;
-  const long long h = (long long)blockIdx.x * PLAN_NT + threadIdx.x;
+  const long long h = vb * PLAN_NT + threadIdx.x;
   long long v = 0;
   if (h < n) {
     const double tot = sc->total_dp;
@@ -245,8 +255,16 @@ __global__ void alloc_kernel(const double *dp, long long n, double beta, double 
     s = red[threadIdx.x];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+    if (threadIdx.x == 0) bsum[vb] = s;
   }
+  __syncthreads();   // red[] is reused by the caller's next block
+}
+
+__global__ void alloc_kernel(const double *dp, long long n, double beta, double ne,
+                             long long uniform_nh, const Scalars *sc, int use_uniform,
+                             long long *n_h, long long *bsum, const int *status) {
+  if (*status & 1) return;
+  alloc_block(blockIdx.x, dp, n, beta, ne, uniform_nh, sc, use_uniform, n_h, bsum);
 }
 
 // Block sums of a host-provided n_h (vpb_set_allocation).
@@ -431,10 +449,9 @@ __global__ void set_iteration_kernel(Sched *sched, int it) { sched->it = it; }
 // values are summed per lane in tile order, then by a fixed xor butterfly,
 // so the result is deterministic (the order differs from a left fold,
 // within the cube-sum tolerance).
-__global__ void fill_fixup_kernel(FillArgs a) {
-  if (*a.status) return;   // failed (now or earlier): the iteration is discarded
+// One warp's 32 consecutive tiles t (lane = t & 31); all 32 lanes call it.
+__device__ void fixup_tiles(const FillArgs &a, long long t) {
   const long long nt = a.sched->ntiles;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool in = t < nt;
   if (in && t == 0 && a.ck_head[0] >= 0) {   // cube begun before this shard
@@ -522,18 +539,22 @@ __global__ void fill_fixup_kernel(FillArgs a) {
   }
 }
 
+__global__ void fill_fixup_kernel(FillArgs a) {
+  if (*a.status) return;   // failed (now or earlier): the iteration is discarded
+  fixup_tiles(a, (long long)blockIdx.x * blockDim.x + threadIdx.x);
+}
+
 // Sum the per-CTA histogram slices in CTA order (deterministic): block
 // (32 elements x 8 partitions); partition p sums its contiguous range of CTA
 // slices in order, then thread p = 0 adds the 8 partials in order.
-__global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
-                                   long long m, double *map_w, long long *map_counts,
-                                   const int *status, const int *gate = nullptr) {
-  __shared__ double sw[8][33];
-  __shared__ long long sc[8][33];
-  if (*status) return;   // failed (now or earlier): the iteration is discarded
-  if (gate != nullptr && *gate == 0) return;   // the fixed-point sums stand (fx_reduce_kernel)
-  const long long i = (long long)blockIdx.x * 32 + threadIdx.x;
-  const int p = threadIdx.y;
+// One 32-interval group (vb) by 256 threads (tx = interval, ty = slice
+// partition); sw/sc: [8][33] shared partials of the calling block.
+__device__ void hist_reduce_group(long long vb, int tx, int ty, double (*sw)[33],
+                                  long long (*sc)[33], const double *hw_part,
+                                  const unsigned *hc_part, int nparts, long long m,
+                                  double *map_w, long long *map_counts) {
+  const long long i = vb * 32 + tx;
+  const int p = ty;
   const int per = (nparts + 7) / 8;
   const int b0 = p * per, b1 = min(nparts, b0 + per);
   double w = 0.0;
@@ -557,16 +578,27 @@ __global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_par
       c += hc_part[(size_t)b * m + i];
     }
   }
-  sw[p][threadIdx.x] = w;
-  sc[p][threadIdx.x] = c;
+  sw[p][tx] = w;
+  sc[p][tx] = c;
   __syncthreads();
   if (p == 0 && i < m) {
-    double t = sw[0][threadIdx.x];
-    long long k = sc[0][threadIdx.x];
-    for (int q = 1; q < 8; q++) { t = __dadd_rn(t, sw[q][threadIdx.x]); k += sc[q][threadIdx.x]; }
+    double t = sw[0][tx];
+    long long k = sc[0][tx];
+    for (int q = 1; q < 8; q++) { t = __dadd_rn(t, sw[q][tx]); k += sc[q][tx]; }
     map_w[i] = t;
     map_counts[i] = k;
   }
+}
+
+__global__ void hist_reduce_kernel(const double *hw_part, const unsigned *hc_part, int nparts,
+                                   long long m, double *map_w, long long *map_counts,
+                                   const int *status, const int *gate = nullptr) {
+  __shared__ double sw[8][33];
+  __shared__ long long sc[8][33];
+  if (*status) return;   // failed (now or earlier): the iteration is discarded
+  if (gate != nullptr && *gate == 0) return;   // the fixed-point sums stand (fx_reduce_kernel)
+  hist_reduce_group(blockIdx.x, threadIdx.x, threadIdx.y, sw, sc, hw_part, hc_part, nparts, m,
+                    map_w, map_counts);
 }
 
 // ---- deterministic mode (vpb_desc flags: VPB_FLAG_DETERMINISTIC) --------
@@ -833,17 +865,12 @@ __device__ double block_pairwise(const double *a, int n, BlockPw &S) {
 constexpr int REFINE_NT = 1024;
 constexpr int REFINE_SMEM_NG = 2048;   // rows up to this length live in smem
 
-__global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const double *map_w,
-                                                          const long long *map_counts, int ng,
-                                                          double alpha, double *scratch,
-                                                          int *status, double *damped_out,
-                                                          int *fx_k = nullptr,
-                                                          int *fx_kmin = nullptr,
-                                                          FxState *fx = nullptr) {
-  extern __shared__ __align__(16) double rsm[];
+__device__ void refine_body(int j, double *rsm, double *edges, const double *map_w,
+                            const long long *map_counts, int ng, double alpha, double *scratch,
+                            int *status, double *damped_out, int *fx_k, int *fx_kmin,
+                            FxState *fx) {
   __shared__ BlockPw S;
   __shared__ int s_skip;
-  const int j = blockIdx.x;
   double *d, *sm, *dw, *cum, *ne, *e;
   if (ng <= REFINE_SMEM_NG) {
     d = rsm; sm = d + ng; dw = sm + ng; cum = dw + ng; ne = cum + ng + 1; e = ne + ng + 1;
@@ -968,8 +995,218 @@ __global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const 
   for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) eg[i] = ne[i];
 }
 
+__global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const double *map_w,
+                                                          const long long *map_counts, int ng,
+                                                          double alpha, double *scratch,
+                                                          int *status, double *damped_out,
+                                                          int *fx_k = nullptr,
+                                                          int *fx_kmin = nullptr,
+                                                          FxState *fx = nullptr) {
+  extern __shared__ __align__(16) double rsm[];
+  refine_body(blockIdx.x, rsm, edges, map_w, map_counts, ng, alpha, scratch, status, damped_out,
+              fx_k, fx_kmin, fx);
+}
+
 inline size_t refine_smem_bytes(int ng) {
   return ng <= REFINE_SMEM_NG ? sizeof(double) * (6 * (size_t)ng + 3) : 0;
+}
+
+// ------------------------------------------------- cooperative update ----
+// The whole post-fill part of an iteration in ONE launch (single GPU, no
+// exchange): cube-chain fixup + histogram reduction | barrier | refinement
+// on CTAs [0, d) concurrently with the fused per-cube terms + pairwise
+// leaves on the others | barrier | pairwise tree (CTA d) | barrier |
+// allocation + plan block sums | the last CTA out ends the iteration.
+// Replaces nine launches (fixup, hist_reduce, cube_terms, results_leaf,
+// results_tree, alloc, refine, end_iteration + the side-stream fork/join)
+// whose launch gaps and single-CTA latencies are most of the non-fill time
+// of small iterations (cfg1).  Opt-in (VPB_COOP=1): on the B200 its phases
+// (globaltimer, cfg1: fixup+reduce 3.7 us, barrier 3.5, terms + leaves 15,
+// tree 9.6, allocation 3.7; refinement 22 us beside them) sum to about the
+// chain's critical path, and the following fill measured 12 us slower, so
+// the chain (with the refinement on a side stream) stays the default.  Launched cooperatively (all CTAs resident),
+// so the spin barriers below cannot deadlock; the same device bodies as the
+// separate kernels, so the results are bitwise those of the launch chain.
+struct UpdArgs {
+  FillArgs fa;                       // fixup (tiles, carries, s1/s2)
+  const double *hw_part;             // histogram slices
+  const unsigned *hc_part;
+  int nparts;
+  long long m;
+  double *map_w;
+  long long *map_counts;
+  const int *hist_gate;              // FX: f64 slices only when gate_f64
+  double *edges;                     // refinement
+  int ng, dims;
+  double alpha;
+  double *refine_scr;
+  int *fx_k, *fx_kmin;
+  FxState *fxs;
+  const double *s1, *s2;             // results
+  const long long *offsets;
+  long long n_cubes;
+  double V, beta;
+  double *d_h, *dp;
+  PwPlanDev pw;
+  double *pwvals, *pwterms;
+  Scalars *sc;
+  double *h_est, *h_var;
+  Sched *sched;
+  int record, tree_flags;
+  double ne;                         // allocation
+  long long uniform_nh;
+  long long *n_h, *bsum;
+  long long nb;
+  int *status, *fail_it;
+  unsigned *bar;                     // [5] barrier counters, zero between launches
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_arrive(unsigned *c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(c, 1u);
+  }
+}
+__device__ __forceinline__ void grid_wait(unsigned *c, unsigned n) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire_u32(c) < n) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+#ifndef VPB_COOP_PROF
+#define VPB_COOP_PROF 0
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#if VPB_COOP_PROF
+#define COOP_TS(k) do { if (threadIdx.x == 0) ts[k] = gtimer(); } while (0)
+#else
+#define COOP_TS(k) do {} while (0)
+#endif
+constexpr int UPD_NT = 1024;   // = PLAN_NT = REFINE_NT
+__global__ void __launch_bounds__(UPD_NT, 1) update_coop_kernel(UpdArgs u) {
+  extern __shared__ __align__(16) unsigned char usm[];
+  __shared__ double sw[4][8][33];
+  __shared__ long long scn[4][8][33];
+  const unsigned G = gridDim.x;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int st0 = *u.status;   // refinement may add its assert bit below, nothing else
+#if VPB_COOP_PROF
+  unsigned long long ts[10] = {0};
+#endif
+  COOP_TS(0);
+  // ---- phase 1: cube chains across tiles || interval histogram slices
+  if (st0 == 0) {
+    const long long nt = u.fa.sched->ntiles;
+    for (long long base = (long long)b * UPD_NT; base < nt; base += (long long)G * UPD_NT)
+      fixup_tiles(u.fa, base + tid);   // whole warps: base + tid covers 32 consecutive tiles
+    if (u.hist_gate == nullptr || *u.hist_gate) {
+      const long long groups = (u.m + 31) / 32;
+      for (long long r = b; r * 4 < groups; r += G) {   // 4 groups of 32 intervals per round
+        const int sub = tid >> 8;
+        hist_reduce_group(r * 4 + sub, tid & 31, (tid >> 5) & 7, sw[sub], scn[sub], u.hw_part,
+                          u.hc_part, u.nparts, u.m, u.map_w, u.map_counts);
+      }
+    }
+  }
+  COOP_TS(1);
+  grid_arrive(u.bar + 0);
+  grid_wait(u.bar + 0, G);
+  COOP_TS(2);
+  if (b < u.dims) {
+    // ---- refinement CTAs: nothing below depends on them; arrive and refine
+    grid_arrive(u.bar + 1);
+    grid_arrive(u.bar + 2);
+    if (st0 == 0)
+      refine_body(b, reinterpret_cast<double *>(usm), u.edges, u.map_w, u.map_counts, u.ng,
+                  u.alpha, u.refine_scr, u.status, nullptr, u.fx_k, u.fx_kmin, u.fxs);
+    COOP_TS(3);
+#if VPB_COOP_PROF
+    if (b == 0 && threadIdx.x == 0)
+      printf("coop refine: p1 %llu b1 %llu refine %llu (ns)\n", ts[1] - ts[0], ts[2] - ts[1],
+             ts[3] - ts[2]);
+#endif
+  } else {
+    const unsigned W = G - u.dims;
+    const int wb = b - u.dims;
+    // ---- per-cube terms (fully parallel: the divisions, sqrt and pow of a
+    // cube do not serialise inside a leaf), then the pairwise leaves; the
+    // barrier between them is among these CTAs only (the refinement CTAs
+    // arrive once, up front)
+    if (!(st0 & 1)) {
+      const bool want_dp = u.beta != 0.0;
+      for (long long h = (long long)wb * UPD_NT + tid; h < u.n_cubes; h += (long long)W * UPD_NT) {
+        double m, t, q;
+        cube_terms(u.s1, u.s2, u.offsets, h, u.V, u.beta, want_dp, u.d_h, u.dp, m, t, q);
+        u.pwterms[h] = m;
+        u.pwterms[u.n_cubes + h] = t;
+        u.pwterms[2 * u.n_cubes + h] = q;
+      }
+    }
+    grid_arrive(u.bar + 4);
+    grid_wait(u.bar + 4, W);
+    if (!(st0 & 1)) {
+      const long long nv = 8LL * u.pw.L;
+      for (long long base = (long long)wb * UPD_NT; base < nv; base += (long long)W * UPD_NT)
+        results_leaf_body(base + tid, u.pwterms, u.n_cubes, u.pw, u.pwvals);
+    }
+    COOP_TS(3);
+    grid_arrive(u.bar + 1);
+    grid_wait(u.bar + 1, G);
+    COOP_TS(4);
+    // ---- pairwise tree: the estimate, variance and allocation total
+    if (wb == 0 && !(st0 & 1))
+      results_tree_body(usm, u.pw, u.pwvals, u.n_cubes, u.V, u.sc, u.h_est, u.h_var, u.sched,
+                        u.record, u.tree_flags);
+    COOP_TS(5);
+    grid_arrive(u.bar + 2);
+    grid_wait(u.bar + 2, G);
+    COOP_TS(6);
+    // ---- allocation for the next iteration + the plan's block sums
+    if (!(st0 & 1))
+      for (long long vb = wb; vb < u.nb; vb += W)
+        alloc_block(vb, u.dp, u.n_cubes, u.beta, u.ne, u.uniform_nh, u.sc, 0, u.n_h, u.bsum);
+    COOP_TS(7);
+#if VPB_COOP_PROF
+    if (wb == 0 && threadIdx.x == 0)
+      printf("coop main: p1 %llu b1 %llu leaves %llu b2 %llu tree %llu b3 %llu alloc %llu (ns)\n",
+             ts[1] - ts[0], ts[2] - ts[1], ts[3] - ts[2], ts[4] - ts[3], ts[5] - ts[4],
+             ts[6] - ts[5], ts[7] - ts[6]);
+#endif
+  }
+  // ---- the last CTA out ends the iteration (vpb end_iteration_kernel) and
+  // re-arms the barriers for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(u.bar + 3, 1u) == G - 1) {
+      __threadfence();
+      const int st = *(volatile int *)u.status;
+      if (st) {
+        if (*u.fail_it < 0) *u.fail_it = u.sched->it;
+      } else {
+        u.sched->it = u.sched->it + 1;
+      }
+      u.bar[0] = 0u; u.bar[1] = 0u; u.bar[2] = 0u; u.bar[3] = 0u; u.bar[4] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+inline size_t update_coop_smem(int ng, const PwPlanDev &pw) {
+  const size_t r = refine_smem_bytes(ng), t = pw_tree_smem(pw);
+  return r > t ? r : t;
 }
 
 // ---------------------------------------------------------- parity kernels --

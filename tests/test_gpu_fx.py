@@ -96,3 +96,18 @@ def test_fx_default_policy(monkeypatch):
     conf = P.IntegratorConfig(n_eval=10 ** 6, max_it=1, n_intervals=1024)
     with P.Integrator("gaussian", [(0.0, 1.0)] * 5, conf, device=0) as it:   # generic kernel
         assert not it.fx_stats()["enabled"]
+
+
+@pytest.mark.parametrize("name,dims,n_eval,its", [("gaussian", 4, 1_000_000, 6),
+                                                  ("multipeak8", 8, 3_000_000, 5)])
+def test_cooperative_update_matches_oracle(monkeypatch, name, dims, n_eval, its):
+    """VPB_COOP=1: the post-fill chain as one cooperative kernel (update.cuh
+    update_coop_kernel) -- same device bodies, same trajectory as the oracle."""
+    monkeypatch.setenv("VPB_COOP", "1")
+    est, var, evals, edges, _ = _run(monkeypatch, name, dims, n_eval, its, n_eval >= 10 ** 6)
+    ref = O.integrate(name, [(0.0, 1.0)] * dims, n_eval, max_it=its, n_intervals=1024,
+                      workers=WORKERS)
+    np.testing.assert_array_equal(evals, ref.evals)
+    np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
+    np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
+    np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=0.0)
