@@ -1123,9 +1123,11 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
     int lg = 0;
     while ((1ll << lg) < cpb) lg++;
     c->fx_L = std::min(52, 62 - lg);
-    c->fx = fx_want && !c->split && !c->records && c->smem_hist && spec &&
-            (layout == LAYOUT_PAIRS || layout == LAYOUT_EDGES) &&
-            c->fx_L >= VPB_FX_T + 6;
+    // (not the split fill: measured on cfg5 -- ~3.4e8 spilled values and two
+    // redos per 11 iterations, 390 vs 344 ms per iteration, and edges 2.4e-12
+    // from the oracle's at 2e6 evaluations)
+    c->fx = fx_want && !c->records && !c->split && c->smem_hist && spec &&
+            (layout == LAYOUT_PAIRS || layout == LAYOUT_EDGES) && c->fx_L >= VPB_FX_T + 4;
     if (c->fx) {
       A(c->fxs, 1);
       A(c->fx_k, m);

@@ -198,6 +198,7 @@ constexpr int LAYOUT_SPLIT = 4;
 constexpr int LAYOUT_FX = 8;
 constexpr int LAYOUT_EDGES_FX = LAYOUT_EDGES | LAYOUT_FX;
 constexpr int LAYOUT_PAIRS_FX = LAYOUT_PAIRS | LAYOUT_FX;
+constexpr int LAYOUT_SPLIT_FX = LAYOUT_SPLIT | LAYOUT_FX;
 #ifndef VPB_FX_T
 #define VPB_FX_T 42   // target: predicted interval average at 2^T units
 #endif
@@ -285,6 +286,52 @@ __host__ __device__ constexpr bool dq_from_table() {
          D >= 3 && D <= 12 && VPB_TABLE_NT > 0;
 }
 
+// FX histogram update of one sample's w2 into DX axes' intervals (flat
+// indices idx = interval * hs + local axis; the CTA's first axis is ax0).
+// Count word = (biased scale exponent << 20) | count, so the count atomic
+// returns the interval's scale 2^k as the high word of a double; y = fma(w2,
+// 2^k, 2^52) holds q = RN(w2 2^k) in its low 52 bits, and (hi:lo) of y is
+// added to the interval's 64-bit (hi:lo) limbs as it is: the low limb's atomic
+// returns the old value for the carry, the high limb gains 0x43300000 per
+// value on top of q's high bits, which fx_reduce_kernel removes exactly from
+// the count.  No selects, no predicates kept across the axes: one max of the
+// high words decides the rare spill path, which takes a too-large value back
+// out (adds 0x43300000:0 - y) and sums it in f64 in global memory instead.
+template <int DX>
+__device__ __forceinline__ void fx_update(const int (&idx)[DX], double w2, unsigned *s_hc,
+                                          unsigned *s_u, int hs, int ng, int ax0,
+                                          const FillArgs &a) {
+  unsigned ow[DX], ql[DX], qh[DX];
+#pragma unroll
+  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_hc[idx[j]], 1u);
+  unsigned mx = 0u;
+#pragma unroll
+  for (int j = 0; j < DX; j++) {
+    const double y = __fma_rn(w2, __hiloint2double((int)(ow[j] & 0xFFF00000u), 0), 0x1p52);
+    ql[j] = (unsigned)__double2loint(y);
+    qh[j] = (unsigned)__double2hiint(y);
+    mx = max(mx, qh[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_u[2 * idx[j]], ql[j]);
+#pragma unroll
+  for (int j = 0; j < DX; j++) atomicAdd(&s_u[2 * idx[j] + 1], addc_u32(qh[j], ow[j], ql[j]));
+  if (mx >= a.fx_lim) {   // rare: q >= 2^L units (or not finite)
+#pragma unroll
+    for (int j = 0; j < DX; j++)
+      if (qh[j] >= a.fx_lim) {
+        const unsigned long long nv =
+            (0x43300000ull << 32) - (((unsigned long long)qh[j] << 32) | ql[j]);
+        const unsigned nl = (unsigned)nv;
+        const unsigned o = atomicAdd(&s_u[2 * idx[j]], nl);
+        atomicAdd(&s_u[2 * idx[j] + 1], addc_u32((unsigned)(nv >> 32), o, nl));
+        const int b = idx[j] / hs, ax = ax0 + idx[j] - b * hs;
+        atomicAdd(a.fx_spill + (size_t)ax * ng + b, w2);
+        atomicAdd(a.fx_nspill, 1ull);
+      }
+  }
+}
+
 template <int ID, int D, int LAYOUT_>
 __host__ __device__ constexpr int fill_nt() {
   constexpr int LAYOUT = LAYOUT_ & 7;
@@ -302,7 +349,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
   constexpr int NT = fill_nt<ID, D, LAYOUT_>();
   constexpr int LAYOUT = LAYOUT_ & 7;
   constexpr bool FX = (LAYOUT_ & LAYOUT_FX) != 0;
-  static_assert(!FX || LAYOUT == LAYOUT_EDGES || LAYOUT == LAYOUT_PAIRS, "FX: edges or pairs");
+  // FX in the split layout (fx_update takes the CTA's axis offset) is not
+  // instantiated: measured slower on cfg5
+  static_assert(!FX || LAYOUT == LAYOUT_EDGES || LAYOUT == LAYOUT_PAIRS || LAYOUT == LAYOUT_SPLIT,
+                "FX: edges, pairs or split");
   if (a.gate != nullptr && *a.gate == 0) return;   // grid-uniform
   constexpr bool PAIRS = LAYOUT == LAYOUT_PAIRS;
   constexpr bool SPLIT = LAYOUT == LAYOUT_SPLIT;
@@ -407,9 +457,11 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
     for (int i = tid; i < hcopies * hs * ng; i += NT) s_hw[i] = 0.0;
     if constexpr (FX) {
       for (int i = tid; i < hs * ng; i += NT) {
-        const int b = i / hs, j = i - b * hs;
-        s_hc[i] = j < d ? (unsigned)fx_biased_exp(__ldg(a.fx_k + (size_t)j * ng + b), fx_e0) << 20
-                        : 0u;
+        const int b = i / hs, j = i - b * hs;   // SPLIT: local axis j is ax0 + j
+        s_hc[i] = j < (SPLIT ? HX : d)
+                      ? (unsigned)fx_biased_exp(__ldg(a.fx_k + (size_t)(ax0 + j) * ng + b), fx_e0)
+                            << 20
+                      : 0u;
       }
     } else {
       for (int i = tid; i < hs * ng; i += NT) s_hc[i] = 0u;
@@ -765,11 +817,15 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
 #pragma unroll
               for (int jl = 0; jl < HX; jl++) idx[jl] = t[jl];
             }
-            double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
+            if constexpr (FX) {
+              fx_update<HX>(idx, w2, s_hc, reinterpret_cast<unsigned *>(s_hw), hs, ng, ax0, a);
+            } else {
+              double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
 #pragma unroll
-            for (int jl = 0; jl < HX; jl++) {
-              atomicAdd(&s_hwl[idx[jl]], w2);
-              atomicAdd(&s_hc[idx[jl]], 1u);
+              for (int jl = 0; jl < HX; jl++) {
+                atomicAdd(&s_hwl[idx[jl]], w2);
+                atomicAdd(&s_hc[idx[jl]], 1u);
+              }
             }
           } else if (RT && a.det == 1) {
             // deterministic mode, pass 1: per (axis, interval) the largest w2
@@ -838,50 +894,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             // the layout changes: the value-returning CAS costs more
             // shared-memory wavefronts than CAST.SPIN, and wavefronts bind.)
             if constexpr (FX) {
-              // fixed point.  Count word = (biased scale exponent << 20) |
-              // count, so the count atomic returns the interval's scale
-              // 2^k as the high word of a double; y = fma(w2, 2^k, 2^52)
-              // holds q = RN(w2 2^k) in its low 52 bits, and (hi:lo) of y is
-              // added to the interval's 64-bit (hi:lo) limbs as it is: the
-              // low limb's atomic returns the old value for the carry, the
-              // high limb gains 0x43300000 per value on top of q's high
-              // bits, which fx_reduce_kernel removes exactly from the count.
-              // No selects, no predicates kept across the axes: one max of
-              // the high words decides the rare spill path, which takes a
-              // too-large value back out (adds 0x43300000:0 - y) and sums it
-              // in f64 in global memory instead.
-              constexpr int DX = D > 0 ? D : 1;
-              unsigned *s_u = reinterpret_cast<unsigned *>(s_hw);
-              unsigned ow[DX], ql[DX], qh[DX];
-#pragma unroll
-              for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_hc[idx[j]], 1u);
-              unsigned mx = 0u;
-#pragma unroll
-              for (int j = 0; j < DX; j++) {
-                const double y =
-                    __fma_rn(w2, __hiloint2double((int)(ow[j] & 0xFFF00000u), 0), 0x1p52);
-                ql[j] = (unsigned)__double2loint(y);
-                qh[j] = (unsigned)__double2hiint(y);
-                mx = max(mx, qh[j]);
-              }
-#pragma unroll
-              for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_u[2 * idx[j]], ql[j]);
-#pragma unroll
-              for (int j = 0; j < DX; j++) atomicAdd(&s_u[2 * idx[j] + 1], addc_u32(qh[j], ow[j], ql[j]));
-              if (mx >= a.fx_lim) {   // rare: q >= 2^L units (or not finite)
-#pragma unroll
-                for (int j = 0; j < DX; j++)
-                  if (qh[j] >= a.fx_lim) {
-                    const unsigned long long nv =
-                        (0x43300000ull << 32) - (((unsigned long long)qh[j] << 32) | ql[j]);
-                    const unsigned nl = (unsigned)nv;
-                    const unsigned o = atomicAdd(&s_u[2 * idx[j]], nl);
-                    atomicAdd(&s_u[2 * idx[j] + 1], addc_u32((unsigned)(nv >> 32), o, nl));
-                    const int b = idx[j] / hs, ax = idx[j] - b * hs;
-                    atomicAdd(a.fx_spill + (size_t)ax * ng + b, w2);
-                    atomicAdd(a.fx_nspill, 1ull);
-                  }
-              }
+              fx_update<(D > 0 ? D : 1)>(idx, w2, s_hc, reinterpret_cast<unsigned *>(s_hw), hs, ng,
+                                         0, a);
             } else {
             // two copies of the sums: the half-warps update different copies,
             // so fewer lanes of one CAS instruction collide on an interval

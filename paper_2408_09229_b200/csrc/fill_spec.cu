@@ -94,26 +94,26 @@ cudaLaunchConfig_t split_config(int grid, size_t smem, cudaStream_t st,
   cfg.numAttrs = 1;
   return cfg;
 }
-template <int ID, int D>
+template <int ID, int D, int L = LAYOUT_SPLIT>
 cudaError_t split_attr() {
   static std::atomic<unsigned long long> done{0};
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT_SPLIT>,
+  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, L>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return e;
   done.fetch_or(bit, std::memory_order_acq_rel);
   return cudaSuccess;
 }
-template <int ID, int D>
+template <int ID, int D, int L>
 cudaError_t launch_split_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
-  cudaError_t e = split_attr<ID, D>();
+  cudaError_t e = split_attr<ID, D, L>();
   if (e != cudaSuccess) return e;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = split_config<ID, D>(grid, smem, st, attr);
-  return cudaLaunchKernelEx(&cfg, fill_kernel<ID, D, LAYOUT_SPLIT>, a);
+  return cudaLaunchKernelEx(&cfg, fill_kernel<ID, D, L>, a);
 }
 template <int ID, int D>
 cudaError_t split_clusters_one(size_t smem, int *clusters) {
@@ -139,7 +139,8 @@ int fill_split_nt(int id, int dims) {
 }
 cudaError_t launch_fill_split(int id, int dims, int grid, size_t smem, cudaStream_t st,
                               const FillArgs &a) {
-#define X(I, D) if (id == I && dims == D) return launch_split_one<I, D>(grid, smem, st, a);
+#define X(I, D) \
+  if (id == I && dims == D) return launch_split_one<I, D, LAYOUT_SPLIT>(grid, smem, st, a);
   VPB_SPLIT_LIST(X)
 #undef X
   return cudaErrorInvalidValue;

@@ -111,3 +111,14 @@ def test_cooperative_update_matches_oracle(monkeypatch, name, dims, n_eval, its)
     np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
     np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
     np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=0.0)
+
+
+
+def test_fx_not_used_by_the_split_fill(monkeypatch):
+    """cfg5's split fill keeps f64 histograms (FX measured slower there)."""
+    monkeypatch.setenv("VPB_HIST_FIXED", "1")
+    monkeypatch.setenv("VPB_FILL_LAYOUT", "split")
+    conf = P.IntegratorConfig(n_eval=2_000_000, max_it=1, n_intervals=1024)
+    with P.Integrator("gaussian20", [(0.0, 1.0)] * 20, conf, device=0) as it:
+        assert it.fill_layout()["layout"].startswith("split")
+        assert not it.fx_stats()["enabled"]
