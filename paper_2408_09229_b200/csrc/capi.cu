@@ -303,6 +303,7 @@ struct vpb_ctx {
   FxState *fxs = nullptr;
   int *fx_k = nullptr, *fx_kmin = nullptr;
   double *fx_spill = nullptr;
+  double *fx_tot = nullptr;    // [d] each axis's w2 row total, last refinement
   // timing
   std::vector<std::array<cudaEvent_t, 6>> ev;  // start, plan, fill k0, fill k1, fill end, end
   cudaEvent_t f0 = nullptr, f1 = nullptr;
@@ -650,7 +651,7 @@ int enqueue_update(vpb_ctx *c, int record) {
   if (!c->side_open) TRY(fork_side(c));
   refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->side>>>(
       c->edges, c->map_w, c->map_counts, c->ng, c->alpha, c->refine_scr, c->status, nullptr,
-      c->fx ? c->fx_k : nullptr, c->fx_kmin, c->fxs);
+      c->fx ? c->fx_k : nullptr, c->fx_kmin, c->fxs, c->fx_tot);
   cube_terms_kernel<<<(unsigned)((c->n_cubes + 255) / 256), 256, 0, c->st>>>(
       c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, c->pwterms, c->status);
   results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
@@ -699,6 +700,7 @@ int enqueue_update_coop(vpb_ctx *c) {
   u.fx_k = c->fx ? c->fx_k : nullptr;
   u.fx_kmin = c->fx_kmin;
   u.fxs = c->fxs;
+  u.fx_tot = c->fx_tot;
   u.s1 = c->s1;
   u.s2 = c->s2;
   u.offsets = c->offsets;
@@ -848,7 +850,7 @@ void free_ctx(vpb_ctx *c) {
                   c->hw_glob, c->hc_part, c->hc_glob, c->status, c->fail_it, c->err_run,
                   c->refine_scr, c->explicit_rb, c->rec_iv, c->rec_w2, c->hw_rec, c->hc_rec,
                   c->ctl, c->bin_k, c->map_q, c->fxs, c->fx_k, c->fx_kmin, c->fx_spill,
-                  c->coop_bar};
+                  c->coop_bar, c->fx_tot};
   for (void *p : ptrs) cached_free(p);
   c->pw.release();
   for (auto &E : c->ev)
@@ -1133,6 +1135,7 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
       A(c->fx_k, m);
       A(c->fx_kmin, (size_t)c->dims);
       A(c->fx_spill, m);
+      A(c->fx_tot, (size_t)c->dims);
     }
   }
   // cooperative update kernel (opt-in, VPB_COOP=1): single GPU,
@@ -1326,6 +1329,7 @@ int vpb_reset(vpb_ctx *c) {
     f.enabled = 1;
     CK(cudaMemcpy(c->fxs, &f, sizeof(f), cudaMemcpyHostToDevice));
     CK(cudaMemset(c->fx_spill, 0, sizeof(double) * (size_t)c->dims * c->ng));
+    CK(cudaMemset(c->fx_tot, 0, sizeof(double) * (size_t)c->dims));
   }
   TRY(uniform_allocation(c));
   CK(cudaStreamSynchronize(c->st));

@@ -203,7 +203,7 @@ constexpr int LAYOUT_SPLIT_FX = LAYOUT_SPLIT | LAYOUT_FX;
 #define VPB_FX_T 42   // target: predicted interval average at 2^T units
 #endif
 #ifndef VPB_FX_P
-#define VPB_FX_P 34   // precision proof: interval sum >= 2^P units per value
+#define VPB_FX_P 38   // precision proof: interval sum >= 2^P units per value
 #endif
 constexpr int FX_K_NONE = 1 << 20;   // no prediction (zero or non-finite average)
 // hi + carry(old + lo): the high limb's addend after the low limb's atomic

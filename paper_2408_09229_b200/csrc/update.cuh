@@ -865,10 +865,23 @@ __device__ double block_pairwise(const double *a, int n, BlockPw &S) {
 constexpr int REFINE_NT = 1024;
 constexpr int REFINE_SMEM_NG = 2048;   // rows up to this length live in smem
 
+// Sum over a block (any order: heuristics only).
+__device__ double block_sum_f64(double v) {
+  __shared__ double part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+  return t;
+}
+
 __device__ void refine_body(int j, double *rsm, double *edges, const double *map_w,
                             const long long *map_counts, int ng, double alpha, double *scratch,
                             int *status, double *damped_out, int *fx_k, int *fx_kmin,
-                            FxState *fx) {
+                            FxState *fx, double *fx_tot) {
   __shared__ BlockPw S;
   __shared__ int s_skip;
   double *d, *sm, *dw, *cum, *ne, *e;
@@ -965,7 +978,19 @@ __device__ void refine_body(int j, double *rsm, double *edges, const double *map
     // of this axis's Jacobian factor (w2 carries (ng dx)^2):
     //   avg' ~ avg_old (dx_new / dx_old)^2,   k = T - ilogb(avg')
     // so that the interval's values sit near 2^T units (the counts per
-    // interval stay ~n/ng: samples are uniform in y)
+    // interval stay ~n/ng: samples are uniform in y).  Trend: the other axes'
+    // maps move too, which scales every interval of this axis alike; the row
+    // total (sum of w2 over all samples) fell by r over the last iteration,
+    // so expect it to fall by about r again (r clamped to [2^-16, 1]: rises
+    // only cost spills, falls cost precision).
+    double rs = 0.0;
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) rs += w[i];
+    rs = block_sum_f64(rs);
+    const double prev_tot = fx_tot[j];
+    double trend = 1.0;
+    if (prev_tot > 0.0 && rs > 0.0) trend = fmin(fmax(rs / prev_tot, 0x1p-16), 1.0);
+    __syncthreads();
+    if (threadIdx.x == 0) fx_tot[j] = rs;
     int kmin = FX_K_NONE;
     for (int i = threadIdx.x; i < ng; i += blockDim.x) {
       const double a0 = i == 0 ? e[0] : ne[i], a1 = i == ng - 1 ? e[ng] : ne[i + 1];
@@ -976,7 +1001,7 @@ __device__ void refine_body(int j, double *rsm, double *edges, const double *map
         if (e[md] <= mid) lo = md; else hi = md - 1;
       }
       const double r = __dadd_rn(a1, -a0) / __dadd_rn(e[lo + 1], -e[lo]);
-      const double pa = d[lo] * r * r;
+      const double pa = d[lo] * r * r * trend;
       const int k = (pa > 0.0 && isfinite(pa)) ? VPB_FX_T - ilogb(pa) : FX_K_NONE;
       fx_k[(size_t)j * ng + i] = k;
       kmin = min(kmin, k);
@@ -1001,10 +1026,11 @@ __global__ void __launch_bounds__(REFINE_NT) refine_kernel(double *edges, const 
                                                           int *status, double *damped_out,
                                                           int *fx_k = nullptr,
                                                           int *fx_kmin = nullptr,
-                                                          FxState *fx = nullptr) {
+                                                          FxState *fx = nullptr,
+                                                          double *fx_tot = nullptr) {
   extern __shared__ __align__(16) double rsm[];
   refine_body(blockIdx.x, rsm, edges, map_w, map_counts, ng, alpha, scratch, status, damped_out,
-              fx_k, fx_kmin, fx);
+              fx_k, fx_kmin, fx, fx_tot);
 }
 
 inline size_t refine_smem_bytes(int ng) {
@@ -1042,6 +1068,7 @@ struct UpdArgs {
   double *refine_scr;
   int *fx_k, *fx_kmin;
   FxState *fxs;
+  double *fx_tot;
   const double *s1, *s2;             // results
   const long long *offsets;
   long long n_cubes;
@@ -1130,7 +1157,7 @@ __global__ void __launch_bounds__(UPD_NT, 1) update_coop_kernel(UpdArgs u) {
     grid_arrive(u.bar + 2);
     if (st0 == 0)
       refine_body(b, reinterpret_cast<double *>(usm), u.edges, u.map_w, u.map_counts, u.ng,
-                  u.alpha, u.refine_scr, u.status, nullptr, u.fx_k, u.fx_kmin, u.fxs);
+                  u.alpha, u.refine_scr, u.status, nullptr, u.fx_k, u.fx_kmin, u.fxs, u.fx_tot);
     COOP_TS(3);
 #if VPB_COOP_PROF
     if (b == 0 && threadIdx.x == 0)
