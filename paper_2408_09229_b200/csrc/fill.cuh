@@ -561,7 +561,13 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
       int cb = rel(__ldg(win + wi)), ce = rel(__ldg(win + wi + 1));
       int seg_beg = 0;
       double v1 = 0.0, v2 = 0.0;
-      unsigned long long k = kk, sl = slot;
+      unsigned long long k = kk;
+      // the batch slot (Philox counter words 2, 3) as two 32-bit halves: when
+      // this lane's n runs neither reach the batch end nor carry into the
+      // high word (nearly always), the low word just counts up; otherwise the
+      // general 64-bit update with the batch wrap (vp/kernels.py:59-62)
+      uint32_t sl_lo = (uint32_t)slot, sl_hi = (uint32_t)(slot >> 32);
+      const bool sl_fast = slot + (unsigned long long)n < batch && sl_lo <= 0xFFFFFFFFu - 16u;
       double dq[DQ_REG ? MAXD : 1];
       uint64_t dpk = 0;   // packed digits (!DQ_REG)
       auto load_digits = [&](int c) {
@@ -658,7 +664,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             const int j = ax0 + jl;
             if ((jl & 1) == 0) {
               const unsigned long long blk = base + (unsigned long long)(j >> 1);
-              philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+              philox((uint32_t)blk, (uint32_t)(blk >> 32), sl_lo, sl_hi, K,
                      w0, w1);
             }
             x[jl] = sample_axis((jl & 1) ? w1 : w0, dq_of(j), nsf2, rns2, a.ngf, ng,
@@ -670,7 +676,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
 #pragma unroll
           for (int k2 = 0; k2 < D / 2; k2++) {
             const unsigned long long blk = base + (unsigned long long)(k2 ^ (xr >> 1));
-            philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+            philox((uint32_t)blk, (uint32_t)(blk >> 32), sl_lo, sl_hi, K,
                    w0, w1);
             const uint64_t wa = (xr & 1) ? w1 : w0, wb = (xr & 1) ? w0 : w1;
             const int s0 = 2 * k2, s1 = s0 + 1;
@@ -688,7 +694,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
         for (int j = 0; j < (D > 0 ? D : d); j++) {
           if ((j & 1) == 0) {
             const unsigned long long blk = base + (unsigned long long)(j >> 1);
-            philox((uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)sl, (uint32_t)(sl >> 32), K,
+            philox((uint32_t)blk, (uint32_t)(blk >> 32), sl_lo, sl_hi, K,
                    w0, w1);
           }
           if constexpr (PAIRS)
@@ -914,7 +920,14 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             }
           }
         }
-        if (++sl == batch) { sl = 0; base += stride_half; }
+        if (__builtin_expect(sl_fast, 1)) {
+          ++sl_lo;
+        } else {
+          unsigned long long s64 = (((unsigned long long)sl_hi << 32) | sl_lo) + 1ull;
+          if (s64 == batch) { s64 = 0; base += stride_half; }
+          sl_lo = (uint32_t)s64;
+          sl_hi = (uint32_t)(s64 >> 32);
+        }
       }
       close_segment(n);
       if constexpr (SPLIT)   // lane 0's remaining swaps (fewer runs in the tile's end)
