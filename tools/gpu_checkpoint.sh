@@ -32,3 +32,8 @@ RX=$(python tools/profile_fill.py cfg4b 5 --probe)
 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
   --kernel-name-base mangled -k "regex:$RX" -c 1 \
   -o gpurun_out/$TAG/p_fill_cfg4b -f python tools/profile_fill.py cfg4b 5 > gpurun_out/$TAG/p_ncu4b.log 2>&1; echo "ncu cfg4b rc=$?"
+# the paper's own breakdown workloads (1e10 evaluations, "def" configuration)
+for f in roos_arnold ridge; do
+  timeout 600 python -m paper_2408_09229_b200 run --integrand $f --config def --n-eval 500000000 \
+    --warmup 1 --format json --out gpurun_out/$TAG/paper_run_${f}_def_1e10.json > /dev/null 2>&1; echo "paper run $f rc=$?"
+done

@@ -35,6 +35,9 @@ for f in sorted(os.listdir(src)):
         if d is not None:
             name = "bench_cfg2.json" if f == "bench_default.json" else f
             json.dump(d, open(os.path.join(dst, name), "w"), indent=1)
+for f in sorted(os.listdir(src)):
+    if f.startswith("paper_run_") and f.endswith(".json"):
+        shutil.copy(os.path.join(src, f), os.path.join(dst, f))
 for f, g in (("p_launches_cfg2.csv", "launches_cfg2.csv"), ("p_launches_cfg1.csv", "launches_cfg1.csv"),
              ("fp64_peak.json", "fp64_peak.json"), ("bench_ref.json", "bench_ref.json"),
              ("tests.log", "gpu_tests.log")):
