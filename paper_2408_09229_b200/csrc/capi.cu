@@ -652,10 +652,8 @@ int enqueue_update(vpb_ctx *c, int record) {
   refine_kernel<<<c->dims, REFINE_NT, refine_smem_bytes(c->ng), c->side>>>(
       c->edges, c->map_w, c->map_counts, c->ng, c->alpha, c->refine_scr, c->status, nullptr,
       c->fx ? c->fx_k : nullptr, c->fx_kmin, c->fxs, c->fx_tot);
-  cube_terms_kernel<<<(unsigned)((c->n_cubes + 255) / 256), 256, 0, c->st>>>(
-      c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, c->pwterms, c->status);
-  results_leaf_kernel<<<(unsigned)((8LL * pd.L + 255) / 256), 256, 0, c->st>>>(
-      c->pwterms, c->n_cubes, pd, c->pwvals, c->status);
+  results_terms_leaf_kernel<<<(unsigned)((pd.L + TL_LEAVES - 1) / TL_LEAVES), 1024, 0, c->st>>>(
+      c->s1, c->s2, c->offsets, c->n_cubes, V, c->beta, c->d_h, c->dp, pd, c->pwvals, c->status);
   const size_t tsm = pw_tree_smem(pd);
   results_tree_kernel<<<1, 1024, tsm, c->st>>>(pd, c->pwvals, c->n_cubes, V, c->sc, c->h_est,
                                                c->h_var, c->sched, c->status, record,
@@ -1896,7 +1894,7 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   pw.build(n);
   TRY(pw.upload());
   struct G { PwPlan *p; ~G() { p->release(); } } g{&pw};
-  DBuf<double> a, b, dh, dp, vals, he, hv, terms;
+  DBuf<double> a, b, dh, dp, vals, he, hv;
   DBuf<long long> doff, hev;
   DBuf<Scalars> sc;
   DBuf<Sched> sch;
@@ -1907,10 +1905,10 @@ int results_common(const double *s1, const double *s2, const int64_t *counts, in
   CK(cudaMemset(st.p, 0, sizeof(int)));
   CK(cudaMemset(sch.p, 0, sizeof(Sched)));
   const double V = 1.0 / (double)n;
-  TRY(terms.alloc(3 * (size_t)n));
-  cube_terms_kernel<<<nblk(n, 256), 256>>>(a.p, b.p, doff.p, n, V, beta, dh.p, dp.p, terms.p,
-                                           st.p);
-  results_leaf_kernel<<<nblk(8LL * pw.L, 256), 256>>>(terms.p, n, pw.dev(), vals.p, st.p);
+  // the iteration's kernel (results_terms_leaf_kernel), so the bitwise
+  // compute_results parity tests pin the code the iteration runs
+  results_terms_leaf_kernel<<<(unsigned)((pw.L + TL_LEAVES - 1) / TL_LEAVES), 1024>>>(
+      a.p, b.p, doff.p, n, V, beta, dh.p, dp.p, pw.dev(), vals.p, st.p);
   const size_t tsm = pw_tree_smem(pw.dev());
   CK(cudaFuncSetAttribute(results_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)PW_TREE_SMEM_MAX));

@@ -62,21 +62,9 @@ __device__ __forceinline__ void cube_terms(const double *s1, const double *s2,
   }
 }
 
-// One thread per cube: the per-cube terms m, rv/c, dp into terms[0|n|2n]
-// (and d_h, dp for the next allocation).  Fully parallel, so the divisions,
-// sqrt and pow do not serialise inside the leaf sums below.
-__global__ void cube_terms_kernel(const double *s1, const double *s2, const long long *offsets,
-                                  long long n, double V, double beta, double *d_h, double *dp,
-                                  double *terms, const int *status) {
-  const long long h = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (h >= n || (*status & 1)) return;
-  double m, t, p;
-  cube_terms(s1, s2, offsets, h, V, beta, beta != 0.0, d_h, dp, m, t, p);
-  terms[h] = m;
-  terms[n + h] = t;
-  terms[2 * n + h] = p;
-}
-
+// numpy's pairwise leaf over precomputed per-cube terms (terms[0|n|2n]): 8
+// lanes per leaf, lane j owns accumulator r[j] -- the cooperative update's
+// second phase (update_coop_kernel)
 __device__ void results_leaf_body(long long gt, const double *terms, long long n, PwPlanDev pw,
                                   double *vals) {
   const int leaf = (int)(gt >> 3), j = (int)(gt & 7);
@@ -109,10 +97,58 @@ __device__ void results_leaf_body(long long gt, const double *terms, long long n
   vals[3 * leaf + 2] = rp;
 }
 
-__global__ void results_leaf_kernel(const double *terms, long long n, PwPlanDev pw, double *vals,
-                                    const int *status) {
+
+// cube_terms_kernel + results_leaf_kernel in one launch without serialising
+// the per-cube divisions/sqrt/pow: 128 threads per leaf (leaves have <= 128
+// cubes) compute one cube's terms each into shared memory, then 8 lanes sum
+// the leaf exactly as results_leaf_body (numpy's 8 accumulators, the fixed
+// combine, the sequential tail).  8 leaves per 1024-thread block.
+constexpr int TL_LEAVES = 8;
+__global__ void __launch_bounds__(1024) results_terms_leaf_kernel(
+    const double *s1, const double *s2, const long long *offsets, long long n, double V,
+    double beta, double *d_h, double *dp, PwPlanDev pw, double *vals, const int *status) {
+  __shared__ double tm[TL_LEAVES][128], tt[TL_LEAVES][128], tp[TL_LEAVES][128];
   if (*status & 1) return;
-  results_leaf_body((long long)blockIdx.x * blockDim.x + threadIdx.x, terms, n, pw, vals);
+  const int slot = threadIdx.x >> 7, e = threadIdx.x & 127;
+  const int leaf = blockIdx.x * TL_LEAVES + slot;
+  const bool live = leaf < pw.L;
+  const long long o = live ? pw.leaf_off[leaf] : 0;
+  const int len = live ? pw.leaf_len[leaf] : 0;
+  if (e < len) {
+    double m, t, q;
+    cube_terms(s1, s2, offsets, o + e, V, beta, beta != 0.0, d_h, dp, m, t, q);
+    tm[slot][e] = m;
+    tt[slot][e] = t;
+    tp[slot][e] = q;
+  }
+  __syncthreads();
+  if (e >= 8) return;   // lanes 0..7 of the leaf's first warp: numpy's accumulators
+  const int j = e;
+  double rm = 0.0, rt = 0.0, rp = 0.0;
+  const int full = len < 8 ? 0 : len - (len % 8);
+  if (len >= 8) {
+    rm = tm[slot][j]; rt = tt[slot][j]; rp = tp[slot][j];
+    for (int i = 8 + j; i < full; i += 8) {
+      rm = __dadd_rn(rm, tm[slot][i]); rt = __dadd_rn(rt, tt[slot][i]);
+      rp = __dadd_rn(rp, tp[slot][i]);
+    }
+  }
+#pragma unroll
+  for (int x = 1; x < 8; x <<= 1) {   // pairs, then quads, then halves (lanes 0-7 only)
+    const double om = __shfl_xor_sync(0xffu, rm, x);
+    const double ot = __shfl_xor_sync(0xffu, rt, x);
+    const double op = __shfl_xor_sync(0xffu, rp, x);
+    rm = __dadd_rn(rm, om); rt = __dadd_rn(rt, ot); rp = __dadd_rn(rp, op);
+  }
+  if (!live || j != 0) return;
+  if (len < 8) { rm = 0.0; rt = 0.0; rp = 0.0; }
+  for (int i = full; i < len; i++) {
+    rm = __dadd_rn(rm, tm[slot][i]); rt = __dadd_rn(rt, tt[slot][i]);
+    rp = __dadd_rn(rp, tp[slot][i]);
+  }
+  vals[3 * leaf + 0] = rm;
+  vals[3 * leaf + 1] = rt;
+  vals[3 * leaf + 2] = rp;
 }
 
 // Generic leaf kernel for a plain array (parity entry point vpb_pairwise_sum).
