@@ -302,6 +302,26 @@ def test_nccl_path_world1_matches_single():
                                [r.estimate for r in b.iterations], rtol=1e-12)
 
 
+def test_nccl_path_world1_with_fixed_point_histograms(monkeypatch):
+    """The in-graph NCCL exchange after the FX fill (fx_reduce writes the
+    rank's map_w before the all-reduce; the predictions come from the
+    reduced map): same trajectory as the single-process run."""
+    import torch.distributed as dist
+    monkeypatch.setenv("VPB_HIST_FIXED", "1")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 200))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        a = integrate("genz_productpeak6", [(0, 1)] * 6, n_eval=2_000_000, max_it=6, seed=5,
+                      distributed=True)
+    finally:
+        dist.destroy_process_group()
+    b = integrate("genz_productpeak6", [(0, 1)] * 6, n_eval=2_000_000, max_it=6, seed=5)
+    assert a.evals_per_iteration == b.evals_per_iteration
+    np.testing.assert_allclose([r.estimate for r in a.iterations],
+                               [r.estimate for r in b.iterations], rtol=1e-12)
+
+
 # ------------------------------------------------- application integrands --
 # pkg/tests/test_integrands.py:114-262 against the device functors
 
