@@ -1025,6 +1025,10 @@ __device__ void refine_body(int j, double *rsm, double *edges, const double *map
     const double prev_tot = fx_tot[j];
     double trend = 1.0;
     if (prev_tot > 0.0 && rs > 0.0) trend = fmin(fmax(rs / prev_tot, 0x1p-16), 1.0);
+    // a row total that jumped up (the first refinement from the uniform map:
+    // x8900 on the three-peak Gaussian) says nothing about the next step --
+    // no prediction, the next iteration stays f64 (instead of a redo)
+    const bool jumped = prev_tot > 0.0 && rs > 4.0 * prev_tot;
     __syncthreads();
     if (threadIdx.x == 0) fx_tot[j] = rs;
     int kmin = FX_K_NONE;
@@ -1050,7 +1054,7 @@ __device__ void refine_body(int j, double *rsm, double *edges, const double *map
     __syncthreads();
     if (threadIdx.x == 0) {
       fx_kmin[j] = s_kmin;
-      atomicAdd(&fx->pred, 1);
+      if (!jumped) atomicAdd(&fx->pred, 1);
     }
   }
   for (int i = 1 + threadIdx.x; i < ng; i += blockDim.x) eg[i] = ne[i];

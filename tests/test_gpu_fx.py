@@ -68,8 +68,10 @@ def test_fx_in_use_on_the_baseline_integrands(monkeypatch, name, dims, n_eval, i
     the first of them is redone (the three-peak Gaussian's map still moves
     by up to 2^8 per interval there), none after."""
     _, _, _, _, st = _run(monkeypatch, name, dims, n_eval, its, True)
-    assert st["fixed_iterations"] == its - 2, st
-    assert st["refilled"] <= (1 if name == "multipeak8" else 0), st
+    # the three-peak Gaussian's first refinement raises the row total 10^4-fold:
+    # no prediction from it, so its fixed point starts at iteration 3
+    assert st["fixed_iterations"] == its - (3 if name == "multipeak8" else 2), st
+    assert st["refilled"] == 0, st
 
 
 @pytest.mark.parametrize("name,dims,n_eval,its", CASES[:2], ids=[c[0] for c in CASES[:2]])
