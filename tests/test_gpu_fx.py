@@ -124,3 +124,28 @@ def test_fx_not_used_by_the_split_fill(monkeypatch):
     with P.Integrator("gaussian20", [(0.0, 1.0)] * 20, conf, device=0) as it:
         assert it.fill_layout()["layout"].startswith("split")
         assert not it.fx_stats()["enabled"]
+
+
+
+@pytest.mark.parametrize("ng,ns,bounds", [(100, None, [(0.0, 1.0)] * 6),
+                                          (1024, 4, [(-1.0, 2.0)] * 6),
+                                          (257, 3, [(0.25, 0.75)] * 6)])
+def test_fx_other_geometries_match_oracle(monkeypatch, ng, ns, bounds):
+    """FX with a coarse map (more runs per interval: a smaller L), a forced
+    stratification and non-unit bounds (the scales follow the intervals'
+    widths in x)."""
+    monkeypatch.setenv("VPB_HIST_FIXED", "1")
+    kw = {} if ns is None else {"n_strat": ns}
+    conf = P.IntegratorConfig(n_eval=2_000_000, max_it=7, n_intervals=ng, **kw)
+    with P.Integrator("genz_oscillatory6", bounds, conf, device=0) as it:
+        it.iterate(7)
+        est, var, evals = it.history()
+        edges = it.edges()
+        st = it.fx_stats()
+    assert st["enabled"] and st["fixed_iterations"] >= 1, st
+    ref = O.integrate("genz_oscillatory6", bounds, 2_000_000, max_it=7, n_intervals=ng,
+                      workers=WORKERS, n_strat=ns)
+    np.testing.assert_array_equal(evals, ref.evals)
+    np.testing.assert_allclose(est, ref.estimates, rtol=1e-10)
+    np.testing.assert_allclose(var, ref.variances, rtol=1e-8)
+    np.testing.assert_allclose(edges, ref.edges, rtol=1e-12, atol=1e-300)
