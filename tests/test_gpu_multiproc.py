@@ -87,11 +87,15 @@ IT_CFG = dict(n_eval=200_000, max_it=4, n_intervals=128, seed=9, batch_size=4096
 NF_BOUNDS = [(0.0, 1.0)] * 9 + [(0.0, 30.0)]
 
 
-def _iterate(bounds, name, distributed):
+FX_CFG = dict(n_eval=2_000_000, max_it=5, n_intervals=1024, seed=9)
+
+
+def _iterate(bounds, name, distributed, cfg=None):
     import paper_2408_09229_b200 as P
-    with P.Integrator(name, bounds, P.IntegratorConfig(**IT_CFG), device=0,
+    cfg = cfg or IT_CFG
+    with P.Integrator(name, bounds, P.IntegratorConfig(**cfg), device=0,
                       distributed=distributed, exchange="host") as it:
-        it.iterate(IT_CFG["max_it"])
+        it.iterate(cfg["max_it"])
         try:
             est, var, ev = it.history()
         except P.NonFiniteIntegrandError as e:
@@ -108,6 +112,9 @@ def _iter_worker(rank, world, port, case, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         if case == "nonfinite":
             q.put((rank, _iterate(NF_BOUNDS, "exponential", True)))
+        elif case == "fx":
+            os.environ["VPB_HIST_FIXED"] = "1"
+            q.put((rank, _iterate([(0.0, 1.0)] * 6, "genz_productpeak6", True, FX_CFG)))
         else:
             q.put((rank, _iterate([(0.0, 1.0)] * 8, "multipeak8", True)))
         dist.barrier()
@@ -120,7 +127,7 @@ def _run_ranks(world, case):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29900 + world * 31 + (os.getpid() % 300) + (7 if case == "nonfinite" else 0)
+    port = 29900 + world * 31 + (os.getpid() % 300) + {"nonfinite": 7, "fx": 13}.get(case, 0)
     procs = [ctx.Process(target=_iter_worker, args=(r, world, port, case, q))
              for r in range(world)]
     for p in procs:
@@ -149,6 +156,25 @@ def test_multiprocess_iterations_match_single(world):
         np.testing.assert_allclose(var, single[2], rtol=1e-8)
         np.testing.assert_allclose(edges, single[4], rtol=1e-12, atol=0)
         # the replicated update leaves every rank with the same map, bitwise
+        assert edges == out[0][4]
+
+
+def test_multiprocess_iterations_with_fixed_point_histograms(monkeypatch):
+    """Each rank fills its shard with the fixed-point histograms (its own
+    proof-or-redo), the host exchange merges the per-rank sums, and the
+    replicated update (and its scale predictions) stays bitwise equal across
+    ranks."""
+    out = _run_ranks(2, "fx")
+    monkeypatch.setenv("VPB_HIST_FIXED", "1")
+    single = _iterate([(0.0, 1.0)] * 6, "genz_productpeak6", False, FX_CFG)
+    assert single[0] == "ok"
+    for r in range(2):
+        kind, est, var, ev, edges, w = out[r]
+        assert kind == "ok" and w == 2, out[r]
+        assert ev == single[3]
+        np.testing.assert_allclose(est, single[1], rtol=1e-10)
+        np.testing.assert_allclose(var, single[2], rtol=1e-8)
+        np.testing.assert_allclose(edges, single[4], rtol=1e-12, atol=0)
         assert edges == out[0][4]
 
 
