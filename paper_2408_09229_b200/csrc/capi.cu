@@ -1456,12 +1456,14 @@ int vpb_fill_layout(vpb_ctx *c, int32_t *layout, int32_t *n_chunks, int32_t *lau
   if (layout) *layout = c->layout;
   if (n_chunks) *n_chunks = c->records ? c->n_chunks : 0;
   // plan_scan, plan_offsets, fill | chunks x (fill + groups), fixup, histogram
-  // reduce, cube_terms, results_leaf, results_tree, alloc, refine, end
+  // reduce, results_terms_leaf, results_tree, alloc, refine, end (+ FX:
+  // fx_begin, the fixed-point fill, fx_reduce; the f64 fill is launched
+  // either way, gated)
   const int n_rec = c->dims - c->rec_k0;
   const int fill = c->records ? c->n_chunks * (1 + (n_rec >= 8) + (n_rec % 8 != 0)) : 1;
   if (launches)
     *launches = c->coop ? 2 + fill + 1 + (c->fx ? 3 : 0)
-                        : 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 3 + 1 + 1 + 1 + (c->fx ? 3 : 0);
+                        : 2 + fill + 2 + (c->rec_k0 > 0 ? 1 : 0) + 2 + 1 + 1 + 1 + (c->fx ? 3 : 0);
   return VPB_OK;
 }
 

@@ -26,7 +26,7 @@ for c in cfg1 cfg3 cfg4a cfg4b cfg5 ra10; do
 done
 bash tools/gpu_profile.sh cfg2 $TAG/p
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/$TAG/p_launches_cfg1.csv python bench.py --config cfg1 --steps 3 --warmup 3 --no-cpu \
+  --log-file gpurun_out/$TAG/p_launches_cfg1.csv python bench.py --config cfg1 --steps 3 --warmup 3 --no-cpu --no-per-function \
   > /dev/null 2>&1; echo "cfg1 launches rc=$?"
 RX=$(python tools/profile_fill.py cfg4b 5 --probe)
 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
