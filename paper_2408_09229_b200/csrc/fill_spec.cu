@@ -3,36 +3,10 @@
 // configurations (cfg1/3: d=4, cfg2: d=8, cfg4: d=6, cfg5: d=20).
 #include <atomic>
 
-#include "fill_launch.h"
+#include "fill_spec_common.h"
 
 namespace vpb {
 
-namespace {
-template <int ID, int D, int LAYOUT>
-cudaError_t launch_one(int grid, size_t smem, cudaStream_t st, const FillArgs &a) {
-  // the max-dynamic-shared-memory attribute is per device: one bit per ordinal
-  static std::atomic<unsigned long long> attr{0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (!(attr.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr.fetch_or(bit, std::memory_order_acq_rel);
-  }
-  fill_kernel<ID, D, LAYOUT><<<grid, (fill_nt<ID, D, LAYOUT>()), smem, st>>>(a);
-  return cudaGetLastError();
-}
-template <int ID, int D, int LAYOUT>
-cudaError_t occ_one(size_t smem, int *ctas) {
-  cudaError_t e = cudaFuncSetAttribute(fill_kernel<ID, D, LAYOUT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, fill_kernel<ID, D, LAYOUT>, fill_nt<ID, D, LAYOUT>(),
-                                                       smem);
-}
-}  // namespace
 
 #define VPB_SPEC_LIST(X)          \
   X(VPB_GAUSSIAN, 4)              \
@@ -54,7 +28,7 @@ int fill_is_specialised(int id, int dims) {
 #define X(I, D) if (id == I && dims == D) return 1;
   VPB_SPEC_LIST(X)
 #undef X
-  return 0;
+  return fill_is_specialised_extra(id, dims);
 }
 
 cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st,
@@ -62,14 +36,15 @@ cudaError_t launch_fill(int id, int dims, int grid, size_t smem, cudaStream_t st
   if (a.det) return launch_fill_generic(id, grid, smem, st, a);   // deterministic mode
 #define X(I, D)                                                                  \
   if (id == I && dims == D) {                                                    \
-    if (a.fx && a.pairs) return launch_one<I, D, LAYOUT_PAIRS_FX>(grid, smem, st, a); \
-    if (a.fx) return launch_one<I, D, LAYOUT_EDGES_FX>(grid, smem, st, a);       \
-    if (a.records) return launch_one<I, D, LAYOUT_RECORDS>(grid, smem, st, a);   \
-    if (a.pairs) return launch_one<I, D, LAYOUT_PAIRS>(grid, smem, st, a);       \
-    if (a.smem_hist) return launch_one<I, D, LAYOUT_EDGES>(grid, smem, st, a);   \
+    if (a.fx && a.pairs) return spec::launch_one<I, D, LAYOUT_PAIRS_FX>(grid, smem, st, a); \
+    if (a.fx) return spec::launch_one<I, D, LAYOUT_EDGES_FX>(grid, smem, st, a);       \
+    if (a.records) return spec::launch_one<I, D, LAYOUT_RECORDS>(grid, smem, st, a);   \
+    if (a.pairs) return spec::launch_one<I, D, LAYOUT_PAIRS>(grid, smem, st, a);       \
+    if (a.smem_hist) return spec::launch_one<I, D, LAYOUT_EDGES>(grid, smem, st, a);   \
   }
   VPB_SPEC_LIST(X)
 #undef X
+  if (fill_is_specialised_extra(id, dims)) return launch_fill_extra(id, dims, grid, smem, st, a);
   if (a.pairs) return cudaErrorInvalidValue;
   return launch_fill_generic(id, grid, smem, st, a);   // incl. global-atomic histograms
 }
@@ -155,12 +130,14 @@ cudaError_t fill_split_clusters(int id, int dims, size_t smem, int *clusters) {
 cudaError_t fill_occupancy(int id, int dims, int layout, size_t smem, int *ctas) {
 #define X(I, D)                                                                  \
   if (id == I && dims == D && layout != LAYOUT_RUNTIME) {                        \
-    if (layout == LAYOUT_RECORDS) return occ_one<I, D, LAYOUT_RECORDS>(smem, ctas); \
-    if (layout == LAYOUT_PAIRS) return occ_one<I, D, LAYOUT_PAIRS>(smem, ctas);  \
-    return occ_one<I, D, LAYOUT_EDGES>(smem, ctas);                              \
+    if (layout == LAYOUT_RECORDS) return spec::occ_one<I, D, LAYOUT_RECORDS>(smem, ctas); \
+    if (layout == LAYOUT_PAIRS) return spec::occ_one<I, D, LAYOUT_PAIRS>(smem, ctas);  \
+    return spec::occ_one<I, D, LAYOUT_EDGES>(smem, ctas);                              \
   }
   VPB_SPEC_LIST(X)
 #undef X
+  if (fill_is_specialised_extra(id, dims) && layout != LAYOUT_RUNTIME)
+    return fill_occupancy_extra(id, dims, layout, smem, ctas);
   if (layout == LAYOUT_PAIRS) return cudaErrorInvalidValue;
   return fill_occupancy_generic(id, smem, ctas);
 }
