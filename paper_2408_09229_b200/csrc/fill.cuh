@@ -383,9 +383,12 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
   // pairwise sums of (x_j - mu_k)^2 are accumulated while the axes are
   // sampled (StreamSum: bit-identical to numpy's row sum of the terms in the
   // order they are sampled), so neither x[] nor the d squared terms per peak
-  // are live across the sampling loop -- up to ~2d(peaks+1) fewer registers
+  // are live across the sampling loop -- up to ~2d(peaks+1) fewer registers.
+  // MP_FMA (the three-peak Gaussian, integrands.cuh VPB_MP_FMA): a running
+  // fma per peak instead of the pairwise tree, in the lane's step order
   constexpr int NPK = ID == VPB_GAUSSIAN ? 1 : (ID == VPB_MULTIPEAK ? 3 : 0);
   constexpr bool STREAM = NPK > 0 && D >= 1 && D <= 128;
+  constexpr bool MP_FMA = VPB_MP_FMA && STREAM && NPK == 3;
   // the Genz functors (cfg4) reduce left to right over the axes in order
   // (never XPERM-permuted): a running dot product / product is the streamed
   // form, bit-identical to integrands.cuh
@@ -638,6 +641,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
         }
         // ---- sample (vp/kernels.py:59-88)
         StreamSum<STREAM ? HX : 1> gacc[NPK > 0 ? NPK : 1];
+        double mpr[NPK > 0 ? NPK : 1];   // MP_FMA: |x - mu_k|^2 by a running fma
         double gz = ID == VPB_GENZ_PRODUCTPEAK ? 1.0 : 0.0;   // GSTREAM running value
         auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
           if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {   // s += x_j a_j
@@ -650,7 +654,8 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
 #pragma unroll
             for (int k = 0; k < NPK; k++) {   // vp/integrands.py:135-139 (x_j - mu_k)^2
               const double u = __dadd_rn(xs, -a.P.p[NPK == 1 ? 0 : 7 + k]);
-              gacc[k].add(step, __dmul_rn(u, u));
+              if constexpr (MP_FMA) mpr[k] = step == 0 ? __dmul_rn(u, u) : __fma_rn(u, u, mpr[k]);
+              else gacc[k].add(step, __dmul_rn(u, u));
             }
           }
         };
@@ -738,6 +743,12 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
         double f;
         if constexpr (STREAM && NPK == 1) {   // integrands.cuh VPB_GAUSSIAN, streamed sum
           f = __dmul_rn(a.P.p[2], fast_exp_nonpos(-div_exact(gsum, a.P.p[3], a.P.p[4])));
+        } else if constexpr (MP_FMA) {
+          double out = 0.0;
+#pragma unroll
+          for (int k = 0; k < NPK; k++)
+            out = __dadd_rn(out, fast_exp_nonpos(__dmul_rn(mpr[k], -a.P.p[5])));
+          f = __dmul_rn(out, __dmul_rn(a.P.p[2], a.P.p[6]));
         } else if constexpr (STREAM) {        // VPB_MULTIPEAK with 3 peaks (host-checked)
           double e[NPK];
 #pragma unroll

@@ -96,7 +96,9 @@ def test_fx_default_policy(monkeypatch):
         assert not it.fx_stats()["enabled"]
     monkeypatch.setenv("VPB_HIST_FIXED", "1")
     conf = P.IntegratorConfig(n_eval=10 ** 6, max_it=1, n_intervals=1024)
-    with P.Integrator("gaussian", [(0.0, 1.0)] * 5, conf, device=0) as it:   # generic kernel
+    from paper_2408_09229_b200 import _native as N
+    assert N.load().vpb_is_specialised(0, 7) == 0
+    with P.Integrator("gaussian", [(0.0, 1.0)] * 7, conf, device=0) as it:   # generic kernel
         assert not it.fx_stats()["enabled"]
 
 

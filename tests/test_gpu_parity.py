@@ -137,6 +137,24 @@ def test_integrand_values(golden):
         np.testing.assert_allclose(v, g[name], rtol=1e-13, atol=atol, err_msg=name)
 
 
+def test_multipeak_fma_form_within_exp_conditioning():
+    # cfg2's three-peak Gaussian runs in the fma form (integrands.cuh
+    # VPB_MP_FMA): each value within ~ulp x (|arg| + 1) of numpy's operation
+    # order, arg = the dominant peak's |x - mu|^2 / (2 sigma^2) (exp's
+    # condition number), on uniform points and points near the middle peak
+    from oracle import integrands_np as I
+    g = np.random.default_rng(3)
+    x = g.random((200_000, 8))
+    x[:100_000] = np.clip(0.5 + 0.05 * g.standard_normal((100_000, 8)), 0.0, 1.0)
+    v = P.lookup("multipeak8").evaluate_batch(x)
+    ref = I.multipeak8(x)
+    mus = np.asarray(I.MP_MUS)
+    arg = np.min(((x[:, None, :] - mus[None, :, None]) ** 2).sum(-1), axis=1) / (2 * I.MP_SIGMA ** 2)
+    ok = ref > 0
+    assert np.all(np.abs(v[ok] - ref[ok]) <= 1e-15 * (arg[ok] + 1.0) * ref[ok])
+    assert np.all(np.abs(v[~ok]) < 1e-300)
+
+
 def test_ridge_recurrence_against_oracle():
     # the blocked window recurrence (integrands.cuh ridge_window) against the
     # oracle's direct sum of exponentials on 200k points, half of them near
