@@ -298,12 +298,17 @@ __host__ __device__ constexpr bool dq_from_table() {
 // high words decides the rare spill path, which takes a too-large value back
 // out (adds 0x43300000:0 - y) and sums it in f64 in global memory instead.
 template <int DX>
-__device__ __forceinline__ void fx_update(const int (&idx)[DX], double w2, unsigned *s_hc,
-                                          unsigned *s_u, int hs, int ng, int ax0,
-                                          const FillArgs &a) {
+__device__ __forceinline__ void fx_update(const int (&idx)[DX], double w2, unsigned *s_fx,
+                                          int hs, int ng, int ax0, const FillArgs &a) {
+  // slot i = [count word, lo limb, hi limb] at s_fx[3i..3i+2]: one address per
+  // axis (IMAD, FMA pipe) for the three atomics, and a 12-byte stride that
+  // spreads a warp's random slots over all 32 banks
+  unsigned *p[DX];
   unsigned ow[DX], ql[DX], qh[DX];
 #pragma unroll
-  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_hc[idx[j]], 1u);
+  for (int j = 0; j < DX; j++) p[j] = s_fx + 3 * idx[j];
+#pragma unroll
+  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(p[j], 1u);
   unsigned mx = 0u;
 #pragma unroll
   for (int j = 0; j < DX; j++) {
@@ -313,9 +318,9 @@ __device__ __forceinline__ void fx_update(const int (&idx)[DX], double w2, unsig
     mx = max(mx, qh[j]);
   }
 #pragma unroll
-  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(&s_u[2 * idx[j]], ql[j]);
+  for (int j = 0; j < DX; j++) ow[j] = atomicAdd(p[j] + 1, ql[j]);
 #pragma unroll
-  for (int j = 0; j < DX; j++) atomicAdd(&s_u[2 * idx[j] + 1], addc_u32(qh[j], ow[j], ql[j]));
+  for (int j = 0; j < DX; j++) atomicAdd(p[j] + 2, addc_u32(qh[j], ow[j], ql[j]));
   if (mx >= a.fx_lim) {   // rare: q >= 2^L units (or not finite)
 #pragma unroll
     for (int j = 0; j < DX; j++)
@@ -323,8 +328,8 @@ __device__ __forceinline__ void fx_update(const int (&idx)[DX], double w2, unsig
         const unsigned long long nv =
             (0x43300000ull << 32) - (((unsigned long long)qh[j] << 32) | ql[j]);
         const unsigned nl = (unsigned)nv;
-        const unsigned o = atomicAdd(&s_u[2 * idx[j]], nl);
-        atomicAdd(&s_u[2 * idx[j] + 1], addc_u32((unsigned)(nv >> 32), o, nl));
+        const unsigned o = atomicAdd(p[j] + 1, nl);
+        atomicAdd(p[j] + 2, addc_u32((unsigned)(nv >> 32), o, nl));
         const int b = idx[j] / hs, ax = ax0 + idx[j] - b * hs;
         atomicAdd(a.fx_spill + (size_t)ax * ng + b, w2);
         atomicAdd(a.fx_nspill, 1ull);
@@ -457,16 +462,19 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
     fx_e0 = 1023 + K;
   }
   if (a.smem_hist) {
-    for (int i = tid; i < hcopies * hs * ng; i += NT) s_hw[i] = 0.0;
-    if constexpr (FX) {
+    if constexpr (FX) {   // [count word, lo, hi] triples over s_hw and s_hc (one copy)
+      unsigned *s_fx = reinterpret_cast<unsigned *>(s_hw);
       for (int i = tid; i < hs * ng; i += NT) {
         const int b = i / hs, j = i - b * hs;   // SPLIT: local axis j is ax0 + j
-        s_hc[i] = j < (SPLIT ? HX : d)
-                      ? (unsigned)fx_biased_exp(__ldg(a.fx_k + (size_t)(ax0 + j) * ng + b), fx_e0)
-                            << 20
-                      : 0u;
+        s_fx[3 * i] = j < (SPLIT ? HX : d)
+                          ? (unsigned)fx_biased_exp(__ldg(a.fx_k + (size_t)(ax0 + j) * ng + b), fx_e0)
+                                << 20
+                          : 0u;
+        s_fx[3 * i + 1] = 0u;
+        s_fx[3 * i + 2] = 0u;
       }
     } else {
+      for (int i = tid; i < hcopies * hs * ng; i += NT) s_hw[i] = 0.0;
       for (int i = tid; i < hs * ng; i += NT) s_hc[i] = 0u;
     }
   }
@@ -835,7 +843,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
               for (int jl = 0; jl < HX; jl++) idx[jl] = t[jl];
             }
             if constexpr (FX) {
-              fx_update<HX>(idx, w2, s_hc, reinterpret_cast<unsigned *>(s_hw), hs, ng, ax0, a);
+              fx_update<HX>(idx, w2, reinterpret_cast<unsigned *>(s_hw), hs, ng, ax0, a);
             } else {
               double *s_hwl = s_hw + (hcopies > 1 ? (size_t)(lane >> 4) * hs * ng : 0);
 #pragma unroll
@@ -911,7 +919,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             // the layout changes: the value-returning CAS costs more
             // shared-memory wavefronts than CAST.SPIN, and wavefronts bind.)
             if constexpr (FX) {
-              fx_update<(D > 0 ? D : 1)>(idx, w2, s_hc, reinterpret_cast<unsigned *>(s_hw), hs, ng,
+              fx_update<(D > 0 ? D : 1)>(idx, w2, reinterpret_cast<unsigned *>(s_hw), hs, ng,
                                          0, a);
             } else {
             // two copies of the sums: the half-warps update different copies,
@@ -1018,9 +1026,9 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
     for (int i = tid; i < nh * ng; i += NT) {   // back to [axis][interval]
       const int j = i / ng, b = i - j * ng;
       if constexpr (FX) {   // the raw (hi:lo) limbs and the count word (with e)
-        reinterpret_cast<unsigned long long *>(hw)[i] =
-            reinterpret_cast<const unsigned long long *>(s_hw)[b * hs + j];
-        hc[i] = s_hc[b * hs + j];
+        const unsigned *t = reinterpret_cast<const unsigned *>(s_hw) + 3 * (b * hs + j);
+        reinterpret_cast<unsigned long long *>(hw)[i] = ((unsigned long long)t[2] << 32) | t[1];
+        hc[i] = t[0];
         continue;
       }
       double v = s_hw[b * hs + j];
