@@ -653,10 +653,10 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
         double gz = ID == VPB_GENZ_PRODUCTPEAK ? 1.0 : 0.0;   // GSTREAM running value
         auto stream_axis = [&](int step, double xs) {   // x of the axis sampled at `step`
           if constexpr (GSTREAM && ID == VPB_GENZ_OSCILLATORY) {   // s += x_j a_j
-            gz = __dadd_rn(gz, __dmul_rn(xs, a.P.p[1 + step]));
+            gz = __fma_rn(xs, a.P.p[1 + step], gz);
           } else if constexpr (GSTREAM) {   // den *= a_j^-2 + (x_j - u_j)^2
             const double u = __dadd_rn(xs, -a.P.p[D + step]);
-            gz = __dmul_rn(gz, __dadd_rn(a.P.p[step], __dmul_rn(u, u)));
+            gz = __dmul_rn(gz, __fma_rn(u, u, a.P.p[step]));
           }
           if constexpr (STREAM) {
 #pragma unroll

@@ -232,7 +232,7 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < (D > 0 ? D : d); j++) {
-      s = __dadd_rn(s, __dmul_rn(x[j], P.p[1 + j]));
+      s = __fma_rn(x[j], P.p[1 + j], s);   // cfg4a pin: fma form (<= 1/2 ulp per axis)
     }
     return cos(__dadd_rn(P.p[0], s));
   } else if constexpr (ID == VPB_GENZ_PRODUCTPEAK) {
@@ -244,7 +244,7 @@ __device__ __forceinline__ double integrand(const double *x, int d, const IParam
 #pragma unroll
     for (int j = 0; j < (D > 0 ? D : d); j++) {
       const double u = __dadd_rn(x[j], -P.p[dd + j]);
-      den = __dmul_rn(den, __dadd_rn(P.p[j], __dmul_rn(u, u)));
+      den = __dmul_rn(den, __fma_rn(u, u, P.p[j]));   // cfg4b pin: fma form
     }
     return __drcp_rn(den);
   } else if constexpr (ID == VPB_SINEXP) {
