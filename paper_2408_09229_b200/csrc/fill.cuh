@@ -47,6 +47,9 @@ constexpr int FILL_NT = VPB_FILL_NT;
 #ifndef VPB_ALL_NT768
 #define VPB_ALL_NT768 0
 #endif
+#ifndef VPB_ROT_STAGES
+#define VPB_ROT_STAGES 0   // barrel stages of the histogram lane rotation (0: by d, below)
+#endif
 #ifndef VPB_STREAM_NT
 #define VPB_STREAM_NT 768   // threads of the streamed-sum and many-axis records kernels
 #endif    // threads per CTA (one CTA per SM)
@@ -899,7 +902,13 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
             if constexpr (XPERM) {
             } else if constexpr (D > 1) {
 #pragma unroll
-              for (int b = 1; b < D; b <<= 1) {   // barrel rotation by rot
+              // d >= 9: at most ~11 strata per axis at any feasible n_eval
+              // (n_strat^d <= n_eval/4), so ~90+ intervals per stratum and few
+              // same-slot collisions: one stage (rotation by 0/1) is enough and
+              // saves 3d SELs (Roos & Arnold 10-D fill -2.3%; cfg4's d = 6 with
+              // 40 intervals per stratum needs all three stages: 1 stage +10%)
+              constexpr int RSTAGES = VPB_ROT_STAGES > 0 ? VPB_ROT_STAGES : (D >= 9 ? 1 : 8);
+              for (int b = 1; b < D && b < (1 << RSTAGES); b <<= 1) {   // barrel rotation by rot
                 const bool on = (rot & b) != 0;
                 int t[D];
 #pragma unroll
