@@ -223,10 +223,59 @@ __device__ __forceinline__ double fast_exp(double x) {
   return fast_exp_core(x);
 }
 
+// Table form (VPB_EXP_TAB, Tang's method): exp(x) = 2^m * 2^(j/32) * exp(r),
+// n = 32m + j = RN(32 x / ln2), |r| <= ln2/64, so exp(r) needs a degree-6
+// Taylor polynomial (truncation 3.5e-18 relative) instead of degree 11: 13
+// FP64 instructions instead of 18, plus one L1-resident gather of
+// RN(2^(j/32)) (256 bytes, read-only path).  Error ~1.5 ulp, like the core
+// form's.  Measured slower (cfg2 fill 3.002 vs 2.942 ms, cfg5 +1%: the
+// gather's latency and registers cost more than the five DFMAs), so off.
+#ifndef VPB_EXP_TAB
+#define VPB_EXP_TAB 0
+#endif
+static __device__ const double kExp2Tab[32] = {
+    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
+    1.0905077326652577, 1.1143867425958924, 1.1387886347566916, 1.1637248587775775,
+    1.189207115002721, 1.215247359980469, 1.241857812073484, 1.2690509571917332,
+    1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
+    1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,
+    1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965,
+    1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,
+    1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002};
+static __constant__ double kExpT[10] = {
+    6755399441055744.0,        // 0: 1.5 * 2^52 shifter
+    46.16624130844683,         // 1: 32/ln2
+    -0x1.62e42fefa0000p-6,     // 2: -ln2/32 hi (36 bits: kd * hi exact for |kd| < 2^17)
+    -5.145609244655338e-14,    // 3: -ln2/32 lo
+    // 4..9: 1/6! .. 1/1!, then 1 (p = fma(p, r, 1))
+    0.001388888888888889, 0.008333333333333333, 0.041666666666666664,
+    0.16666666666666666, 0.5, 1.0};
+__device__ __forceinline__ double fast_exp_tab(double x) {   // x in [-1400, 1400]
+  double kd = __fma_rn(x, kExpT[1], kExpT[0]);
+  const int n = __double2loint(kd);
+  const double t = __ldg(kExp2Tab + (n & 31));   // issued early, used last
+  kd = __dadd_rn(kd, -kExpT[0]);
+  double r = __fma_rn(kd, kExpT[2], x);
+  r = __fma_rn(kd, kExpT[3], r);
+  double p = kExpT[4];
+#pragma unroll
+  for (int i = 5; i <= 9; i++) p = __fma_rn(p, r, kExpT[i]);
+  p = __fma_rn(p, r, 1.0);
+  const int m = n >> 5;   // floor(n / 32)
+  const int m1 = m >> 1, m2 = m - m1;
+  const double s1 = __longlong_as_double((long long)(m1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(m2 + 1023) << 52);
+  return __dmul_rn(__dmul_rn(__dmul_rn(p, t), s1), s2);
+}
+
 // exp of a finite, non-positive argument (Gaussian exponents of finite
 // points): one DMNMX clamp.
 __device__ __forceinline__ double fast_exp_nonpos(double x) {
+#if VPB_EXP_TAB
+  return fast_exp_tab(fmax(x, -kExp[16]));
+#else
   return fast_exp_core(fmax(x, -kExp[16]));
+#endif
 }
 
 // 32-bit unsigned division by a runtime-constant divisor D in [1, 2^31]
