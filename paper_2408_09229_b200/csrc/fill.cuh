@@ -257,16 +257,21 @@ __host__ __device__ constexpr bool axis_symmetric() {
 // StreamSum keeps few partials live) and the many-axis records kernels --
 // they fit 80 registers and gain from the sixth warp per scheduler (cfg2
 // -1.3%, cfg1 -7%, cfg4 -5..7%, cfg5 -3%, cfg3 ridge -1% fill time), or
-// 1024 in table mode (below); the rest keep 640.
+// a per-integrand count in table mode (below); the rest keep 640.
 // Table mode: RN(digit/N) read from the shared digit table instead of d
-// registers, which brings these kernels to 64 registers and 1024 threads
-// (32 warps per SM).  Measured fill time: Genz oscillatory -4.8% (cfg4a),
-// product peak -2.3% (cfg4b), Roos & Arnold -8.5%, linear -7.8%, Morokoff
-// -3.9%, exponential -3.3%, path integral -3.0%; cosine (+0.9%, its cos
-// spills) and the streamed Gaussians (cfg1/cfg2 +3-5%: their table reads
-// compete with the pair table) keep the digits in registers.
+// registers.  Round 1 (f64 CAS histograms) ran every table-mode kernel at
+// 64 registers and 1024 threads.  Re-measured with the fixed-point
+// histograms (round 2, alternating A/B, tools/ab_pair.sh / ab_registry.sh,
+// fill time against 1024 threads): Roos & Arnold -7.4%, linear -7.5%,
+// exponential -4.7% at 640 threads (96 registers); Morokoff -2.8%, path
+// integral -2.2% at 768 (80); the Ridge (cfg3) stays at 1024 (640: +3.2%);
+// and the Genz pair (cfg4a/b) is fastest out of table mode altogether, with
+// the digits in registers at 768 threads (-2.9% / -4.0%).  Cosine (its cos
+// spills) and the streamed Gaussians (cfg1/cfg2: their table reads compete
+// with the pair table) keep the digits in registers.
+// VPB_TABLE_NT: -1 per integrand as above, > 0 one count for all, 0 off.
 #ifndef VPB_TABLE_NT
-#define VPB_TABLE_NT 1024
+#define VPB_TABLE_NT -1
 #endif
 #ifndef VPB_REC_NT
 #define VPB_REC_NT VPB_STREAM_NT
@@ -280,13 +285,25 @@ __host__ __device__ constexpr bool axis_symmetric() {
 #ifndef VPB_TABLE_MULTIPEAK
 #define VPB_TABLE_MULTIPEAK 0
 #endif
+#ifndef VPB_TABLE_GENZ
+#define VPB_TABLE_GENZ 0
+#endif
 template <int ID, int D>
 __host__ __device__ constexpr bool dq_from_table() {
-  return (ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_ROOS_ARNOLD ||
+  return (((ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK) && VPB_TABLE_GENZ) ||
+          ID == VPB_ROOS_ARNOLD ||
           (ID == VPB_MULTIPEAK && VPB_TABLE_MULTIPEAK) ||
           ID == VPB_LINEAR || ID == VPB_EXPONENTIAL || ID == VPB_MOROKOFF ||
           ID == VPB_PATH_INTEGRAL || (ID == VPB_RIDGE && VPB_TABLE_RIDGE)) &&
-         D >= 3 && D <= 12 && VPB_TABLE_NT > 0;
+         D >= 3 && D <= 12 && VPB_TABLE_NT != 0;
+}
+// threads per CTA of a table-mode kernel
+template <int ID>
+__host__ __device__ constexpr int table_nt() {
+  return VPB_TABLE_NT > 0 ? VPB_TABLE_NT
+         : (ID == VPB_RIDGE || ID == VPB_GENZ_OSCILLATORY || ID == VPB_GENZ_PRODUCTPEAK) ? 1024
+         : (ID == VPB_MOROKOFF || ID == VPB_PATH_INTEGRAL)                               ? 768
+                                                                                         : 640;
 }
 
 // FX histogram update of one sample's w2 into DX axes' intervals (flat
@@ -344,7 +361,7 @@ template <int ID, int D, int LAYOUT_>
 __host__ __device__ constexpr int fill_nt() {
   constexpr int LAYOUT = LAYOUT_ & 7;
   return (LAYOUT == LAYOUT_SPLIT)                    ? VPB_SPLIT_NT
-         : dq_from_table<ID, D>()                    ? VPB_TABLE_NT
+         : dq_from_table<ID, D>()                    ? table_nt<ID>()
          : (LAYOUT == LAYOUT_RECORDS && D > 12)      ? VPB_REC_NT
          : ((ID == VPB_GAUSSIAN || ID == VPB_MULTIPEAK || ID == VPB_GENZ_OSCILLATORY ||
              ID == VPB_GENZ_PRODUCTPEAK || ID == VPB_RIDGE || VPB_ALL_NT768) &&
