@@ -41,7 +41,9 @@ namespace vpb {
 #define VPB_FILL_NT 640
 #endif
 #ifndef VPB_FILL_RPT
-#define VPB_FILL_RPT 16   // measured: 8 and 32 lose on cfg1/cfg2 (32: cfg4 -1%, cfg1 +69%)
+#define VPB_FILL_RPT 16   // measured: 8 and 32 lose on cfg1/cfg2 (32: cfg4 -1%, cfg1 +69%;
+                          // round 2 with FX: 32 gives cfg4a/b -1.9/-2.1%, cfg2/cfg5 0,
+                          // cfg1 +65% -- it would have to be a per-plan choice)
 #endif
 constexpr int FILL_NT = VPB_FILL_NT;
 #ifndef VPB_ALL_NT768
