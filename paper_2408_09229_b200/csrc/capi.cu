@@ -259,6 +259,7 @@ struct vpb_ctx {
   // fill launch geometry
   int grid = 0;
   int grid_tiles = 0;          // tile walkers (CTAs, or 2-CTA clusters for the split fill)
+  int rpt = FILL_RPT;          // runs per lane per warp tile (Sched.rpt; choose_rpt)
   bool split = false;          // LAYOUT_SPLIT
   bool smem_hist = true;
   bool pairs = false;
@@ -340,7 +341,7 @@ FillArgs fill_args(vpb_ctx *c) {
   a.seed = c->seed;
   a.keys = PhiloxKeys(c->seed);
   a.nsdiv = MagicDiv((uint32_t)c->ns);
-  const unsigned long long step = (unsigned long long)c->grid_tiles * FILL_TILE;
+  const unsigned long long step = (unsigned long long)c->grid_tiles * (32ull * c->rpt);
   a.dk = (long long)(step / (unsigned long long)c->batch);
   a.ds = (long long)(step % (unsigned long long)c->batch);
   a.sched = c->sched;
@@ -1084,6 +1085,18 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
                      : (c->smem_hist && spec) ? LAYOUT_EDGES
                                               : LAYOUT_RUNTIME;
   c->layout = layout;
+  // Runs per lane per warp tile: 32 for large plans (the per-tile work --
+  // cube search, segment closing, carries -- amortised over twice the runs:
+  // cfg4a/b fill -1.9/-2.1%, cfg2/cfg5 neutral), 16 below ~3e7 evaluations
+  // per rank, where 32-run tiles leave warps idle (cfg1: +65%), and for the
+  // records layout (hist.cuh maps record slots with the compile-time tile).
+  // VPB_RPT=16|32 forces it.
+  // (c->records covers the generic kernel's records mode too)
+  c->rpt = (!c->records && d->n_eval >= 30000000ll) ? 32 : FILL_RPT;
+  if (const char *e = std::getenv("VPB_RPT")) {
+    const int v = std::atoi(e);
+    if ((v == 16 || v == 32) && !c->records) c->rpt = v;
+  }
   // a records-layout fill with d >= 12 histograms its first REC_K0 axes in
   // the shared memory left next to the edges (fill.cuh K0)
   if (layout == LAYOUT_RECORDS && c->dims >= 12) {
@@ -1312,6 +1325,7 @@ int vpb_reset(vpb_ctx *c) {
   TRY(upload_uniform_edges(c));
   Sched s{};
   s.it = 0;   // end_iteration_kernel advances it
+  s.rpt = c->rpt;
   CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
   Scalars z{};
   CK(cudaMemcpy(c->sc, &z, sizeof(z), cudaMemcpyHostToDevice));
@@ -1810,7 +1824,7 @@ int vpb_fill_host(const int64_t *offsets, int64_t n_cubes, const double *edges, 
   s.run_base = run_base;
   s.lo = run_lo;
   s.hi = run_hi;
-  s.ntiles = (run_hi - run_lo + FILL_TILE - 1) / FILL_TILE;
+  s.ntiles = (run_hi - run_lo + 32ll * c->rpt - 1) / (32ll * c->rpt);
   CK(cudaMemcpy(c->sched, &s, sizeof(s), cudaMemcpyHostToDevice));
   // rebuild the tile table for the explicit range (block prefixes still in bsum)
   plan_offsets_kernel<<<(unsigned)c->nb, PLAN_NT, 0, c->st>>>(c->n_h, c->n_cubes, c->bsum,

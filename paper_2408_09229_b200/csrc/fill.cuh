@@ -41,9 +41,9 @@ namespace vpb {
 #define VPB_FILL_NT 640
 #endif
 #ifndef VPB_FILL_RPT
-#define VPB_FILL_RPT 16   // measured: 8 and 32 lose on cfg1/cfg2 (32: cfg4 -1%, cfg1 +69%;
-                          // round 2 with FX: 32 gives cfg4a/b -1.9/-2.1%, cfg2/cfg5 0,
-                          // cfg1 +65% -- it would have to be a per-plan choice)
+#define VPB_FILL_RPT 16   // the default / small-plan runs per lane; large plans take 32
+                          // per context (Sched.rpt, capi.cu: cfg4a/b -2.1/-2.4%, cfg2
+                          // -1.3%, cfg5 0; 32 on cfg1's small plan: +65%)
 #endif
 constexpr int FILL_NT = VPB_FILL_NT;
 #ifndef VPB_ALL_NT768
@@ -74,8 +74,10 @@ struct Sched {
   long long total;        // plan.total
   long long run_base_next;
   int it;                 // 0-based iteration index being processed
-  int pad;
+  int rpt;                // runs per lane per warp tile (0: FILL_RPT); set per context
 };
+// runs per lane of a schedule: 16, or 32 for large plans (capi.cu choose_rpt)
+__host__ __device__ inline int sched_rpt(const Sched &s) { return s.rpt > 0 ? s.rpt : FILL_RPT; }
 
 struct FillArgs {
   const long long *offsets;     // [n_cubes+1]
@@ -542,10 +544,13 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
   const long long ncl = SPLIT ? (long long)(gridDim.x >> 1) : (long long)gridDim.x;
   const long long t_beg = tL + (long long)warp * P + cid;
   const long long t_end = min(tL + (long long)(warp + 1) * P, tU);
-  const long long rec0 = lo + tL * FILL_TILE;   // run of record 0 (records mode)
+  // runs per lane / per warp tile of this schedule (records mode: FILL_RPT)
+  const int rpt = sched_rpt(S);
+  const long long tile_runs = 32ll * rpt;
+  const long long rec0 = lo + tL * tile_runs;   // run of record 0 (records mode)
   // (k, slot) of this lane's first run in its first tile; advanced per grid stride
-  unsigned long long g0 = (unsigned long long)(S.run_base + lo + t_beg * FILL_TILE +
-                                               (long long)lane * FILL_RPT);
+  unsigned long long g0 = (unsigned long long)(S.run_base + lo + t_beg * tile_runs +
+                                               (long long)lane * rpt);
   unsigned long long kk = g0 / batch, slot = g0 % batch;
   // SPLIT: one swap of per-run partials with the partner CTA's same lane
   // (slot = step parity; the same number of steps in both CTAs)
@@ -564,19 +569,19 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
   };
 
   for (long long tile = t_beg; tile < t_end; tile += ncl) {
-    const long long T0 = lo + tile * FILL_TILE;
-    const long long T1 = min(T0 + (long long)FILL_TILE, hi);
+    const long long T0 = lo + tile * tile_runs;
+    const long long T1 = min(T0 + tile_runs, hi);
     const long long c_first = a.tile_cube[tile];
     const long long c_last = a.tile_cube[tile + 1];
     const int nwin = (int)(c_last - c_first + 2);
     const long long *win = a.offsets + c_first;   // the tile's cube offsets (L1-resident)
 
-    const long long r0 = T0 + (long long)lane * FILL_RPT;
-    const long long r1 = min(r0 + (long long)FILL_RPT, T1);
+    const long long r0 = T0 + (long long)lane * rpt;
+    const long long r1 = min(r0 + (long long)rpt, T1);
     SegItem H{-1, 0.0, 0.0}, T{-1, 0.0, 0.0};
     int t_through = 0;
     // SPLIT: every lane takes part in lane 0's number of swaps
-    const int nsteps = (int)min((long long)FILL_RPT, T1 - T0);
+    const int nsteps = (int)min((long long)rpt, T1 - T0);
 
     if (r0 < r1) {
       // cube of r0: largest i with win[i] <= r0
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
       }
       // run positions relative to r0 in 32-bit registers (cube bounds clamped
       // to [-1, RPT+1], which keeps every comparison below exact)
-      auto rel = [&](long long v) { return (int)max(min(v - r0, (long long)FILL_RPT + 1), -1ll); };
+      auto rel = [&](long long v) { return (int)max(min(v - r0, (long long)rpt + 1), -1ll); };
       const int n = (int)(r1 - r0);
       int wi = lo_i;
       int cube = (int)c_first + wi;
@@ -1023,7 +1028,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
     const unsigned any_head = __ballot_sync(0xffffffffu, head_carry);
     if (lane == 0 && any_head == 0 && (!SPLIT || crank == 0)) a.ck_head[tile] = -1;
     // ---- the tile's last lane with runs publishes the tail carry
-    const int last = (int)((T1 - T0 + FILL_RPT - 1) / FILL_RPT) - 1;
+    const int last = (int)((T1 - T0 + rpt - 1) / rpt) - 1;
     if (lane == last && (!SPLIT || crank == 0)) {
       if (T.key >= 0) {
         a.ck_tail[tile] = T.key;

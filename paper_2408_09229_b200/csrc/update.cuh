@@ -423,7 +423,8 @@ __global__ void plan_scan_kernel(long long *bsum, long long nb, Sched *sched, in
     s.total = total;
     s.lo = lo;
     s.hi = hi;
-    s.ntiles = (s.hi - s.lo + FILL_TILE - 1) / FILL_TILE;
+    const long long tr = 32ll * sched_rpt(s);
+    s.ntiles = (s.hi - s.lo + tr - 1) / tr;
     if (s.ntiles > ntiles_cap) { atomicOr(status, 2); s.ntiles = 0; }
     *sched = s;
     if (record) hist_evals[s.it] = total;
@@ -450,8 +451,9 @@ __global__ void plan_offsets_kernel(const long long *n_h, long long n, const lon
     const long long a = beg > lo ? beg : lo, b = end < hi ? end : hi;
     if (a < b) {
       // tiles whose first run lies in [a, b)
-      t0 = (a - lo + FILL_TILE - 1) / FILL_TILE;
-      t1 = (b - lo + FILL_TILE - 1) / FILL_TILE;
+      const long long tr = 32ll * sched_rpt(*sched);
+      t0 = (a - lo + tr - 1) / tr;
+      t1 = (b - lo + tr - 1) / tr;
       if (b == hi) tile_cube[sched->ntiles] = (int)h;   // sentinel: cube of the last run
     }
   }
