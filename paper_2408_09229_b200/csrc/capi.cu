@@ -1090,12 +1090,12 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // cfg4a/b fill -1.9/-2.1%, cfg2/cfg5 neutral), 16 below ~3e7 evaluations
   // per rank, where 32-run tiles leave warps idle (cfg1: +65%), and for the
   // records layout (hist.cuh maps record slots with the compile-time tile).
-  // VPB_RPT=16|32 forces it.
+  // VPB_RPT=8|16|32|64 forces it.
   // (c->records covers the generic kernel's records mode too)
   c->rpt = (!c->records && d->n_eval >= 30000000ll) ? 32 : FILL_RPT;
   if (const char *e = std::getenv("VPB_RPT")) {
     const int v = std::atoi(e);
-    if ((v == 16 || v == 32) && !c->records) c->rpt = v;
+    if ((v == 8 || v == 16 || v == 32 || v == 64) && !c->records) c->rpt = v;
   }
   // a records-layout fill with d >= 12 histograms its first REC_K0 axes in
   // the shared memory left next to the edges (fill.cuh K0)

@@ -605,7 +605,7 @@ __global__ void __launch_bounds__((fill_nt<ID, D, LAYOUT_>()), 1) fill_kernel(co
       // high word (nearly always), the low word just counts up; otherwise the
       // general 64-bit update with the batch wrap (vp/kernels.py:59-62)
       uint32_t sl_lo = (uint32_t)slot, sl_hi = (uint32_t)(slot >> 32);
-      const bool sl_fast = slot + (unsigned long long)n < batch && sl_lo <= 0xFFFFFFFFu - 16u;
+      const bool sl_fast = slot + (unsigned long long)n < batch && sl_lo <= 0xFFFFFFFFu - (uint32_t)n;
       double dq[DQ_REG ? MAXD : 1];
       uint64_t dpk = 0;   // packed digits (!DQ_REG)
       auto load_digits = [&](int c) {
