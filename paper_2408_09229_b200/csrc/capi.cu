@@ -1085,14 +1085,19 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
                      : (c->smem_hist && spec) ? LAYOUT_EDGES
                                               : LAYOUT_RUNTIME;
   c->layout = layout;
-  // Runs per lane per warp tile: 32 for large plans (the per-tile work --
-  // cube search, segment closing, carries -- amortised over twice the runs:
-  // cfg4a/b fill -1.9/-2.1%, cfg2/cfg5 neutral), 16 below ~3e7 evaluations
-  // per rank, where 32-run tiles leave warps idle (cfg1: +65%), and for the
-  // records layout (hist.cuh maps record slots with the compile-time tile).
-  // VPB_RPT=8|16|32|64 forces it.
-  // (c->records covers the generic kernel's records mode too)
-  c->rpt = (!c->records && d->n_eval >= 30000000ll) ? 32 : FILL_RPT;
+  // Runs per lane per warp tile: more for large plans (the per-tile work --
+  // cube search, segment closing, carries -- amortised over more runs).
+  // Measured against 16 (one box, alternating): 32 gives cfg4a/b fill
+  // -2.1/-2.4%, cfg2 -1.3%; 64 another -1.1/-1.2% and -0.5%, but +0.4% on
+  // the split fill (cfg5), which keeps 32.  Below ~3e7 evaluations per
+  // iteration long tiles leave warps idle (cfg1 at 32: +65%), and the
+  // records layout maps its record slots with the compile-time 16 (c->records
+  // covers the generic kernel's records mode too).  VPB_RPT=8|16|32|64
+  // forces it.
+  c->rpt = c->records                                 ? FILL_RPT
+           : (d->n_eval >= 100000000ll && !c->split) ? 64
+           : d->n_eval >= 30000000ll                 ? 32
+                                                     : FILL_RPT;
   if (const char *e = std::getenv("VPB_RPT")) {
     const int v = std::atoi(e);
     if ((v == 8 || v == 16 || v == 32 || v == 64) && !c->records) c->rpt = v;

@@ -42,8 +42,7 @@ namespace vpb {
 #endif
 #ifndef VPB_FILL_RPT
 #define VPB_FILL_RPT 16   // the default / small-plan runs per lane; large plans take 32
-                          // per context (Sched.rpt, capi.cu: cfg4a/b -2.1/-2.4%, cfg2
-                          // -1.3%, cfg5 0; 32 on cfg1's small plan: +65%)
+                          // or 64 per context (Sched.rpt, capi.cu)
 #endif
 constexpr int FILL_NT = VPB_FILL_NT;
 #ifndef VPB_ALL_NT768

@@ -436,3 +436,28 @@ def test_nonfinite_integrand_reports_point():
 def test_python_callable_rejected():
     with pytest.raises(P.ContractViolationError):
         P.integrate(lambda x: x.sum(axis=1), [(0, 1)] * 2, n_eval=1000, batched=True)
+
+
+@pytest.mark.parametrize("rpt", ["16", "32", "64"])
+def test_fill_slot_low_word_wrap_matches_oracle(monkeypatch, rpt):
+    """The Philox batch slot (counter words 2-3, vp/kernels.py:59-62) crossing
+    2^32 inside a lane's runs, and the batch end right after it: the fill's
+    32-bit slot fast path must hand over to the 64-bit update in time, for
+    16, 32 and 64 runs per lane (capi.cu: Sched.rpt)."""
+    monkeypatch.setenv("VPB_RPT", rpt)
+    name, dims, ng, ns = "genz_productpeak6", 6, 100, 2
+    g = np.random.default_rng(77)
+    off = _random_plan(g, ns, dims, 200, 2000)
+    edges = np.sort(g.random((dims, ng + 1)), axis=1)
+    edges[:, 0], edges[:, -1] = 0.0, 1.0
+    # a seed per case: vpb_fill_host's cached context is keyed on it (and
+    # picks its runs per lane at creation)
+    seed, batch = 4242 + int(rpt), (1 << 32) + 7
+    rb = (1 << 32) - 40            # slot low word 0xFFFFFFD8 at the first run
+    got = ops.parallel_fill(off, edges, ns, seed, batch, name, run_base=rb)
+    ref = O.fill(off, edges, ns, seed, batch, rb, name, workers=os.cpu_count() or 1)
+    np.testing.assert_array_equal(got[1], ref[1])
+    np.testing.assert_array_equal(got[4], ref[4])
+    np.testing.assert_allclose(got[0], ref[0], rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(got[2], ref[2], rtol=1e-12, atol=1e-290)
+    np.testing.assert_allclose(got[3], ref[3], rtol=1e-12, atol=1e-290)
