@@ -1094,7 +1094,9 @@ int vpb_create(const vpb_desc *d, vpb_ctx **out) {
   // records layout maps its record slots with the compile-time 16 (c->records
   // covers the generic kernel's records mode too).  VPB_RPT=8|16|32|64
   // forces it.
-  c->rpt = c->records                                 ? FILL_RPT
+  // The Ridge (cfg3: ~2000 FP64 operations per run) keeps 16: its long
+  // runs make the grid's last tiles the tail (64: +6% on cfg3).
+  c->rpt = (c->records || c->id == VPB_RIDGE)          ? FILL_RPT
            : (d->n_eval >= 100000000ll && !c->split) ? 64
            : d->n_eval >= 30000000ll                 ? 32
                                                      : FILL_RPT;
